@@ -1,0 +1,509 @@
+#!/usr/bin/env python
+"""bench.py — SpGEMM GFlop/s (2×products/s) and HBM roofline fraction on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--strategy hybrid|precise]
+    python bench.py --impl reference ...      # the CPU oracle on a bounded sample (baseline arm)
+
+One step = one pass of the whole hot path (stages 1-4: spgemm_symbolic + spgemm_numeric)
+over the workload's A and B, which are resident in HBM before timing starts.  L2 is
+flushed (a 512 MiB memset) before every timed step, outside the timed window.  Each step
+is bracketed by CUDA events on the library's stream; the K step times are summed.  For
+N > 1 (torchrun) every rank runs its row block through the dist_* ABI and the step time
+is the max over ranks.  Rank 0 prints one JSON line.
+
+metric = 2·Σu / t  (flops = 2·nnz(Ĉ) [P:433]); the compulsory-byte HBM fraction of the
+step and the roofline of the dominant kernel are reported next to it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "SpGEMM GFlop/s (2x products/s) and HBM GB/s vs roofline at 1/2/4/8 B200"
+CONFIGS = {
+    "c1": "C = A·A, A = 2D 5-point Laplacian on a 32×32 grid (1024 rows, fp64 CSR)",
+    "c2": "C = A·A, A = 3D 27-point stencil on a 128³ grid (2.1M rows, FEM-like)",
+    "c3a": "C = A·A, A = R-MAT scale 22, edge factor 16, (0.45,0.15,0.15,0.25), permuted",
+    "c3b": "C = A·A, A = R-MAT Graph500 skew (0.57,0.19,0.19,0.05), scale 18, edge factor 16",
+    "c4a": "Galerkin R·(A·P), A = 3D 7-point 256³, tentative 2×2×2 aggregation P",
+    "c4b": "Galerkin R·(A·P), A = 3D 7-point 256³, Jacobi-smoothed aggregation P (ω=3/4)",
+    "c5": "C = A·B, A = band(64) n=2^23, B = 64 uniform columns per row",
+}
+SMI_REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
+               "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown", "display_clock_setting"]
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+# ----------------------------------------------------------------------------- inputs
+def make_workload(cfg: str, scale: int | None = None):
+    """Returns a list of (name, A, B) products; B None means B = A."""
+    import gen
+    if cfg == "c1":
+        return [("A2", gen.stencil("2d5", 32), None)]
+    if cfg == "c2":
+        return [("A2", gen.stencil("3d27", scale or 128), None)]
+    if cfg == "c3a":
+        return [("A2", gen.rmat(scale or 22, 16, (0.45, 0.15, 0.15, 0.25), seed=gen.SEED, mode="real"), None)]
+    if cfg == "c3b":
+        return [("A2", gen.rmat(scale or 18, 16, (0.57, 0.19, 0.19, 0.05), seed=gen.SEED, mode="real"), None)]
+    if cfg in ("c4a", "c4b"):
+        n = scale or 256
+        A = gen.stencil("3d7", n)
+        P = gen.aggregation_P(n, smoothed=(cfg == "c4b"))
+        R = gen.transpose(P)
+        return [("AP", A, P), ("R(AP)", R, "prev")]
+    if cfg == "c5":
+        n = 1 << (scale or 23)
+        return [("AB", gen.band(n), gen.uniform_rows(n, n, 64))]
+    raise SystemExit("unknown config %s" % cfg)
+
+
+def csr_bytes(rows, nnz):
+    return 8 * (rows + 1) + 12 * nnz
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw,utilization.gpu"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 5:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16),
+                                         float(parts[3]), float(parts[4])))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        load = [s for s in self.samples if s[4] > 0] or self.samples
+        sm = sorted(s[0] for s in load)
+        mask = 0
+        for s in load:
+            mask |= s[2]
+        reasons = [n for b, n in enumerate(SMI_REASONS) if mask & (1 << b) and n != "gpu_idle"]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in load), "reasons": reasons,
+                "samples": len(load)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1504_05022_b200 as sg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("--gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    flags = sg.FLAG_PRECISE if args.strategy == "precise" else 0
+    work = make_workload(args.config, args.scale)
+    stream = torch.cuda.Stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    lib = sg.load()
+
+    # inputs resident in HBM
+    dev_inputs = []
+    prev_is_out = False
+    for name, A, B in work:
+        dA = sg.DeviceCsr.from_host(A)
+        dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
+        dev_inputs.append((name, A, B, dA, dB))
+        prev_is_out = prev_is_out or isinstance(B, str)
+    torch.cuda.synchronize()
+
+    uid = None
+    if world > 1:
+        obj = [sg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    def one_step(collect=False):
+        """Whole hot path once: every product of the workload, symbolic + numeric."""
+        out = None
+        info = []
+        for (name, A, B, dA, dB) in dev_inputs:
+            Bm = dA if dB is None else (out if isinstance(dB, str) else dB)
+            if world == 1:
+                op = sg.SpGEMM(dA, Bm, flags, stream)
+                nnz = op.symbolic()
+                out = op.numeric()
+                if collect:
+                    info.append((name, op.stats(), nnz, dA, Bm))
+                op.destroy()
+            else:
+                op = sg.DistSpGEMM(rank, world, uid, dA.rows, dA.cols, Bm.cols, dA, Bm,
+                                   flags | sg.FLAG_INPUTS_REPLICATED, stream)
+                rb, re_, ln, gn = op.symbolic()
+                blk = op.numeric()
+                if collect:
+                    info.append((name, op.stats(), gn, dA, Bm))
+                op.destroy()
+                out = blk  # multi-stage chains on N>1 are not supported (c4 runs at N=1)
+        return out, info
+
+    if world > 1 and len(dev_inputs) > 1:
+        raise SystemExit("chained workloads (c4) run at --gpus 1 only")
+
+    # warm-up (also warms the stream-ordered pool)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one_step()
+    torch.cuda.synchronize()
+    _, info = one_step(collect=True)
+    torch.cuda.synchronize()
+
+    def timed_pass():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = []
+        with ClockSampler(local) as cs:
+            for _ in range(args.steps):
+                flush.zero_()  # L2 flush outside the timed window (512 MiB > 126 MB L2)
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                torch.cuda.current_stream().wait_stream(stream)
+                stream.wait_stream(torch.cuda.current_stream())
+                s.record(stream)
+                with torch.cuda.stream(stream):
+                    one_step()
+                e.record(stream)
+                ev.append((s, e))
+            torch.cuda.synchronize()
+        ms = sum(s.elapsed_time(e) for s, e in ev)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, cs.summary()
+
+    ms_total, clocks = timed_pass()
+    if any(r in BAD_REASONS for r in clocks["reasons"]) or (
+            clocks["sm_mhz"] and clocks["sm_max_mhz"] and clocks["sm_mhz"] < 0.5 * clocks["sm_max_mhz"]
+            and not clocks["reasons"]):
+        ms_total, clocks2 = timed_pass()  # re-measure once
+        clocks = dict(clocks2, remeasured=True, first_reasons=clocks["reasons"])
+    ms_step = ms_total / args.steps
+
+    # ---------------- per-step accounting (from the collected pass) ----------------
+    sum_u = sum(st["sum_u"] if world == 1 else 0 for _, st, _, _, _ in info)
+    if world > 1:
+        # Σu over the whole problem: every rank sums its local Σu, then all-reduce
+        loc = torch.tensor([sum(st["sum_u"] for _, st, _, _, _ in info)], dtype=torch.int64, device="cuda")
+        dist.all_reduce(loc)
+        sum_u = int(loc.item())
+    cb = 0
+    nnz_c_tot = 0
+    launches = 0
+    for name, st, nnz_c, dA, Bm in info:
+        m = dA.rows
+        cb += csr_bytes(m, dA.nnz) + csr_bytes(Bm.rows, Bm.nnz) + csr_bytes(m, nnz_c)
+        nnz_c_tot += nnz_c
+        launches += st["launches_symbolic"] + st["launches_numeric"]
+    gflops = 2.0 * sum_u / (ms_step * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    step_gbs = cb / (ms_step * 1e-3) / 1e9
+
+    # dominant kernel: the stage-3 class launch with the largest time in the collected pass
+    name0, st0, nnz0, dA0, Bm0 = max(info, key=lambda x: max((c["ms"] for c in x[1]["classes"].values()), default=0))
+    cls_name, cls = max(st0["classes"].items(), key=lambda kv: kv[1]["ms"])
+    hybrid = args.strategy == "hybrid"
+    # algorithmic bytes of one launch of that class: row pointers of A
+    # (16 B/row) + perm/offsets/nnz (20 B/row) + the class's A entries (12 B) + B read once
+    # (12 B per entry, at most one per product) + the class's output entries (12 B)
+    alg = (36 * cls["rows"] + 12 * cls["a_entries"] + 12 * min(Bm0.nnz, cls["products"]) +
+           (12 * cls["c_entries"] if hybrid else 0))
+    kern = "stage3 class %s (%s)" % (cls_name, "k_group" if cls_name.startswith("g") else
+                                    "k_warp_hash" if cls_name.startswith("w") else
+                                    "k_cta_hash" if cls_name.startswith("c") else "k_long")
+    # the live timing of that class comes from the library's CUDA events on its stream
+    achieved = alg / (cls["ms"] * 1e-3) / 1e9 if cls["ms"] > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            key = "%s/%s/%s" % (args.config, args.strategy, cls_name)
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+
+    # ---------------- end-to-end through the public API with host buffers ----------------
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        e2e = e2e_measure(args, work, flags, stream, sum_u)
+
+    result = {
+        "metric": METRIC,
+        "value": round(gflops, 3),
+        "unit": "GFlop/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generators, gen/; %s)" % ("coef values" if args.config in ("c1", "c2", "c4a", "c4b")
+                                                            else "real values"),
+        "config": {"workload": "%s: %s" % (args.config, CONFIGS[args.config]),
+                   "strategy": args.strategy, "sum_u": sum_u, "nnz_c": nnz_c_tot,
+                   "nnz_a": int(sum(d[3].nnz for d in dev_inputs)),
+                   "parallelism": "row blocks x%d (dist_* ABI, NCCL)" % world if world > 1 else "1 GPU",
+                   "l2": "flushed before every timed step (512 MiB memset, outside the timed window)",
+                   "scale": args.scale},
+        "hbm": {"compulsory_bytes": cb, "achieved_gbs": round(step_gbs, 1),
+                "frac_of_peak": round(step_gbs / hbm_peak, 4), "peak_gbs": hbm_peak,
+                "peak_source": peak_src},
+        "roofline": {"bound": "hbm", "kernel": kern,
+                     "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
+                     "traffic": traffic, "alg_bytes_per_launch": int(alg),
+                     "launch_ms": round(cls["ms"], 4), "peak_source": peak_src},
+        "stage_ms": {n: [round(x, 4) for x in st["stage_ms"]] for n, st, _, _, _ in info},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    if e2e:
+        result["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(args, work, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_measure(args, work, flags, stream, sum_u):
+    """Same metric through the public API with pinned HOST buffers: H2D of the step's
+    inputs, the four stages, D2H of C — all inside the timed window."""
+    import torch
+
+    import paper_1504_05022_b200 as sg
+
+    def pin(a, dt):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dt).pin_memory()
+
+    host = []
+    h2d = 0
+    for name, A, B in work:
+        hA = (pin(A.rp, torch.int64), pin(A.ci, torch.int32), pin(A.val, torch.float64), A.shape)
+        h2d += csr_bytes(A.shape[0], A.nnz)
+        hB = None
+        if B is not None and not isinstance(B, str):
+            hB = (pin(B.rp, torch.int64), pin(B.ci, torch.int32), pin(B.val, torch.float64), B.shape)
+            h2d += csr_bytes(B.shape[0], B.nnz)
+        host.append((hA, hB, B))
+
+    def todev(h):
+        rp, ci, val, shape = h
+        return sg.DeviceCsr(shape[0], shape[1], rp.to("cuda", non_blocking=True), ci.to("cuda", non_blocking=True),
+                            val.to("cuda", non_blocking=True))
+
+    d2h_holder = {}
+
+    def step():
+        out = None
+        d2h = 0
+        for hA, hB, B in host:
+            dA = todev(hA)
+            dB = dA if B is None else (out if isinstance(B, str) else todev(hB))
+            op = sg.SpGEMM(dA, dB, flags, stream)
+            nnz = op.symbolic()
+            out = op.numeric()
+            op.destroy()
+        # result back to the host (pinned)
+        key = out.ci.numel()
+        if key not in d2h_holder:
+            d2h_holder.clear()
+            d2h_holder[key] = (torch.empty(out.rp.numel(), dtype=torch.int64).pin_memory(),
+                               torch.empty(out.ci.numel(), dtype=torch.int32).pin_memory(),
+                               torch.empty(out.val.numel(), dtype=torch.float64).pin_memory())
+        hr, hc, hv = d2h_holder[key]
+        hr.copy_(out.rp, non_blocking=True)
+        hc.copy_(out.ci, non_blocking=True)
+        hv.copy_(out.val, non_blocking=True)
+        d2h += csr_bytes(out.rows, out.ci.numel())
+        return d2h
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, min(args.warmup, 2))):
+            step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    tot = 0.0
+    d2h = 0
+    for _ in range(steps):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        with torch.cuda.stream(stream):
+            d2h = step()
+        e.record(stream)
+        torch.cuda.synchronize()
+        tot += s.elapsed_time(e)
+    ms = tot / steps
+    return {"value": round(2.0 * sum_u / (ms * 1e-3) / 1e9, 3), "unit": "GFlop/s", "ms_per_step": round(ms, 3),
+            "steps": steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "note": "pinned host buffers; H2D of A (and B) + symbolic + numeric + D2H of C per step"}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def _row_sample(A, budget_products):
+    """Contiguous row block [0, r) of A with at most budget_products products (A·A)."""
+    import oracle
+    u, _ = oracle.upper_bound(A, A, 0, min(A.shape[0], 1 << 22))
+    cs = np.cumsum(u)
+    r = int(np.searchsorted(cs, budget_products)) + 1
+    return max(1, min(r, A.shape[0])), int(cs[min(r, len(cs)) - 1])
+
+
+def cpu_baseline(args, work, budget_s=15.0):
+    """The oracle (oracle/, never tuned for this) on the host cores over a bounded sample:
+    a leading block of rows of the first product, sized to ~budget_s seconds."""
+    import oracle
+    threads = oracle.max_threads()
+    name, A, B = work[0]
+    Bm = A if B is None else B
+    if isinstance(Bm, str):
+        Bm = A
+    # calibrate on a small block, then run ~budget_s of work
+    u_all, _ = oracle.upper_bound(A, Bm)
+    cs = np.cumsum(u_all)
+    r_small = int(min(A.shape[0], max(1, np.searchsorted(cs, 2e7) + 1)))
+    t0 = time.perf_counter()
+    oracle.spgemm(A, Bm, 0, r_small, with_bound=False, threads=threads)
+    t_small = time.perf_counter() - t0
+    rate = cs[r_small - 1] / max(t_small, 1e-6)
+    r = int(min(A.shape[0], max(r_small, np.searchsorted(cs, rate * budget_s) + 1)))
+    t0 = time.perf_counter()
+    oracle.spgemm(A, Bm, 0, r, with_bound=False, threads=threads)
+    t = time.perf_counter() - t0
+    prods = int(cs[r - 1])
+    cpu = ""
+    try:
+        cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        pass
+    return {"value": round(2.0 * prods / t / 1e9, 4), "unit": "GFlop/s", "cores": threads, "kind": "oracle",
+            "sample": "rows [0, %d) of %s product %s (%d products, %.1f s)" % (r, args.config, name, prods, t),
+            "cpu": cpu}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (the baseline arm)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # under torchrun only rank 0 works
+    import oracle
+    work = make_workload(args.config, args.scale)
+    name, A, B = work[0]
+    Bm = A if B is None or isinstance(B, str) else B
+    threads = oracle.max_threads()
+    u_all, sum_u = oracle.upper_bound(A, Bm)
+    cs = np.cumsum(u_all)
+    # per step: a bounded sample sized so warmup+steps finish in a few minutes
+    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    r_small = int(min(A.shape[0], max(1, np.searchsorted(cs, 2e7) + 1)))
+    t0 = time.perf_counter()
+    oracle.spgemm(A, Bm, 0, r_small, with_bound=False, threads=threads)
+    rate = cs[r_small - 1] / max(time.perf_counter() - t0, 1e-6)
+    r = int(min(A.shape[0], max(r_small, np.searchsorted(cs, rate * per_step_s) + 1)))
+    prods = int(cs[r - 1])
+    for _ in range(args.warmup):
+        oracle.spgemm(A, Bm, 0, r_small, with_bound=False, threads=threads)
+    t = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.spgemm(A, Bm, 0, r, with_bound=False, threads=threads)
+        t += time.perf_counter() - t0
+    ms = t / args.steps * 1e3
+    v = 2.0 * prods / (ms * 1e-3) / 1e9
+    sample = "rows [0, %d) of %s product %s (%d of %d products)" % (r, args.config, name, prods, sum_u)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GFlop/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "%s: %s" % (args.config, CONFIGS[args.config]), "sample": sample},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFlop/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--scale", type=int, default=None, help="override the config's size parameter")
+    ap.add_argument("--strategy", default="hybrid", choices=["hybrid", "precise"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

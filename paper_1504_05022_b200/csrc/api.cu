@@ -1,0 +1,705 @@
+// api.cu — the C ABI of libspgemm.so (include/spgemm.h): handle, workspace, and the
+// host orchestration of the four stages (Figure "framework", [P:187-196]).
+//
+// symbolic:  stage 1 + stage 2 (GPU) → one small D2H of the per-class counts (the host-side
+//            bin counters of [P:264]: kernels are issued only for non-empty classes) →
+//            allocate C~ (hybrid) → stage 3 per class → long rows with the progressive
+//            growth loop ([P:297]) → scan of nnz(c_i*) → D2H of nnz(C) ([P:301]).
+// numeric:   stage 4 copy C~ → C (hybrid), or stage 3 again straight into C (PRECISE).
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace sg;
+
+namespace {
+
+thread_local std::string t_last_error;
+int g_force_tier = -1;
+int64_t g_long_cap0 = 16384;
+int64_t g_long_threshold = 0;
+
+__global__ void k_tier_to_i32(const uint8_t* t, int32_t* o, int64_t m) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) o[i] = t[i];
+}
+
+__global__ void k_iota(int32_t* p, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int32_t)i;
+}
+
+__global__ void k_long_slots(const LongState* st, int64_t n, int64_t* slots) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) slots[i] = 2 * st[i].cap;
+}
+
+// PRECISE numeric: exact long-row tables (cap = nnz(c_i*) from the symbolic pass).
+__global__ void k_long_exact(LongState* st, const int32_t* perm, int64_t first, int64_t n,
+                             const int64_t* nnz_row, const int64_t* arp, int64_t* slots) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int row = perm[first + i];
+  int64_t c = nnz_row[row];
+  if (c < 1) c = 1;
+  st[i].cap = c;
+  st[i].capmax = c;
+  st[i].count = 0;
+  st[i].next_a = arp[row];
+  st[i].done = 0;
+  slots[i] = 2 * c;
+}
+
+__global__ void k_class_sums(int64_t m, const uint8_t* __restrict__ tier, const int64_t* __restrict__ U,
+                             const int64_t* __restrict__ arp, const int64_t* __restrict__ nnz_row,
+                             unsigned long long* out) {
+  __shared__ unsigned long long s[3 * NUM_TIERS];
+  for (int i = threadIdx.x; i < 3 * NUM_TIERS; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    const int t = tier[i];
+    atomicAdd(&s[t], (unsigned long long)(arp[i + 1] - arp[i]));
+    atomicAdd(&s[NUM_TIERS + t], (unsigned long long)U[i]);
+    atomicAdd(&s[2 * NUM_TIERS + t], (unsigned long long)nnz_row[i]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * NUM_TIERS; i += blockDim.x)
+    if (s[i]) atomicAdd(&out[i], s[i]);
+}
+
+}  // namespace
+
+spgemm_status_t sg_dist_destroy(spgemm_handle_t h);
+bool sg_is_dist(spgemm_handle_t h);
+const char* sg_dist_error(spgemm_handle_t h);
+spgemm_status_t sg_dist_stats(spgemm_handle_t h, spgemm_stats_t* out);
+
+struct spgemm_handle_s {
+  uint64_t magic = 0x53494e474c45ull;  // "SINGLE"; dist handles carry another tag here
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t flags = 0;
+  int64_t m = 0, k = 0, n = 0, a_nnz = 0, b_nnz = 0;
+  CsrView A{}, B{};
+  std::vector<std::pair<void*, size_t>> allocs;  // symbolic workspace
+  size_t bytes = 0;
+  Stage12Ws ws{};
+  int64_t* nnz_row = nullptr;
+  int64_t* c_rp = nullptr;
+  int64_t* scan_tmp = nullptr;
+  int32_t* ctil_col = nullptr;
+  double* ctil_val = nullptr;
+  int64_t* pinned = nullptr;  // host pinned scratch [kSumLen + 8]
+  // long rows
+  int64_t nlong = 0, long_first = 0;
+  LongState* lst = nullptr;
+  int32_t** lkeys = nullptr;
+  double** lvals = nullptr;
+  int32_t** lold_keys = nullptr;
+  double** lold_vals = nullptr;
+  int64_t* lold_slots = nullptr;
+  int32_t* lact = nullptr;
+  int32_t* lovf = nullptr;
+  int32_t* lovf_cnt = nullptr;
+  int32_t* liota = nullptr;
+  int64_t* lslots = nullptr;
+  int64_t* lslot_off = nullptr;
+  int64_t long_entries = 0;
+  int32_t growth_rounds = 0;
+  int64_t tier_count[NUM_TIERS] = {};
+  int64_t tier_off[NUM_TIERS + 1] = {};
+  int64_t sum_u = 0, max_u = 0, sum_cap = 0;
+  bool sym_ok = false;
+  int64_t nnz_c = 0;
+  std::string err;
+  cudaEvent_t ev[6] = {};
+  cudaEvent_t tev[NUM_TIERS][2] = {};
+  bool tev_used[NUM_TIERS] = {};
+  int32_t launches_sym = 0, launches_num = 0;
+  bool ev_ok = false;
+  bool numeric_recorded = false;
+};
+
+namespace {
+
+spgemm_status_t fail(spgemm_handle_t h, spgemm_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  t_last_error = buf;
+  return s;
+}
+
+spgemm_status_t cuda_fail(spgemm_handle_t h, cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(h, SPGEMM_ERROR_OUT_OF_MEMORY, "%s: out of device memory", where);
+  }
+  return fail(h, SPGEMM_ERROR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(h, call)                                   \
+  do {                                                \
+    cudaError_t _e = (call);                          \
+    if (_e != cudaSuccess) return cuda_fail(h, _e, #call); \
+  } while (0)
+
+template <typename T>
+spgemm_status_t dalloc(spgemm_handle_t h, T** p, int64_t count) {
+  const size_t bytes = sizeof(T) * size_t(count > 0 ? count : 1);
+  void* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, bytes, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMallocAsync");
+  h->allocs.emplace_back(q, bytes);
+  h->bytes += bytes;
+  *p = static_cast<T*>(q);
+  return SPGEMM_SUCCESS;
+}
+
+#define AL(h, p, n)                                   \
+  do {                                                \
+    spgemm_status_t _s = dalloc(h, p, n);             \
+    if (_s != SPGEMM_SUCCESS) return _s;              \
+  } while (0)
+
+void free_symbolic(spgemm_handle_t h) {
+  for (auto& a : h->allocs) cudaFreeAsync(a.first, h->stream);
+  h->allocs.clear();
+  h->bytes = 0;
+  h->ws = Stage12Ws{};
+  h->nnz_row = h->c_rp = h->scan_tmp = nullptr;
+  h->ctil_col = nullptr;
+  h->ctil_val = nullptr;
+  h->lst = nullptr;
+  h->lkeys = h->lold_keys = nullptr;
+  h->lvals = h->lold_vals = nullptr;
+  h->nlong = 0;
+  h->long_entries = 0;
+  h->growth_rounds = 0;
+  h->sym_ok = false;
+  h->numeric_recorded = false;
+}
+
+spgemm_status_t sync(spgemm_handle_t h) {
+  CK(h, cudaStreamSynchronize(h->stream));
+  return SPGEMM_SUCCESS;
+}
+
+int env_int(const char* name, int def) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : def;
+}
+
+// Allocate tables for the long rows listed in `list` (device, nlist entries) whose slot
+// counts are in h->lslots[0..nlist); assign pointers (moving the current ones to old_*).
+spgemm_status_t long_alloc_tables(spgemm_handle_t h, const int32_t* list, int64_t nlist, bool fill,
+                                  bool keep_old) {
+  CK(h, launch_exclusive_scan(h->lslots, h->lslot_off, nlist, h->scan_tmp, h->stream));
+  CK(h, cudaMemcpyAsync(h->pinned, h->lslot_off + nlist, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  spgemm_status_t s = sync(h);
+  if (s != SPGEMM_SUCCESS) return s;
+  const int64_t total = h->pinned[0];
+  int32_t* kb = nullptr;
+  double* vb = nullptr;
+  AL(h, &kb, total);
+  if (fill) AL(h, &vb, total);
+  h->long_entries += total / 2;
+  CK(h, launch_long_assign(list, nlist, h->lslot_off, kb, vb, h->lkeys, h->lvals,
+                           keep_old ? h->lold_keys : nullptr, keep_old ? h->lold_vals : nullptr,
+                           h->lold_slots, h->lst, h->stream));
+  return SPGEMM_SUCCESS;
+}
+
+// Long-row path: progressive allocation with checkpoint / 2x growth / relaunch ([P:297]).
+spgemm_status_t run_long(spgemm_handle_t h, int mode) {
+  const int64_t nl = h->nlong;
+  if (nl == 0) return SPGEMM_SUCCESS;
+  const bool fill = mode == MODE_FILL;
+  AL(h, &h->lst, nl);
+  AL(h, &h->lkeys, nl);
+  AL(h, &h->lvals, nl);
+  AL(h, &h->lold_keys, nl);
+  AL(h, &h->lold_vals, nl);
+  AL(h, &h->lold_slots, nl);
+  AL(h, &h->lact, nl);
+  AL(h, &h->lovf, nl);
+  AL(h, &h->liota, nl);
+  AL(h, &h->lovf_cnt, 1);
+  AL(h, &h->lslots, nl);
+  AL(h, &h->lslot_off, nl + 1);
+  CK(h, cudaMemsetAsync(h->lkeys, 0, sizeof(int32_t*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lvals, 0, sizeof(double*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_vals, 0, sizeof(double*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_slots, 0, sizeof(int64_t) * nl, h->stream));
+  const unsigned g = (unsigned)((nl + 255) / 256);
+  k_iota<<<g, 256, 0, h->stream>>>(h->liota, nl);
+  const int64_t cap0 = (h->flags & SPGEMM_FLAG_UPPER_BOUND) ? INT64_MAX / 4 : g_long_cap0;
+  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, cap0, h->A, h->B, h->stream));
+  k_long_slots<<<g, 256, 0, h->stream>>>(h->lst, nl, h->lslots);
+  spgemm_status_t s = long_alloc_tables(h, h->liota, nl, fill, false);
+  if (s != SPGEMM_SUCCESS) return s;
+  CK(h, cudaMemcpyAsync(h->lact, h->liota, sizeof(int32_t) * nl, cudaMemcpyDeviceToDevice, h->stream));
+  int64_t nactive = nl;
+  for (int round = 0;; ++round) {
+    CK(h, cudaMemsetAsync(h->lovf_cnt, 0, sizeof(int32_t), h->stream));
+    LongArgs la{};
+    la.A = h->A;
+    la.B = h->B;
+    la.n = h->n;
+    la.perm = h->ws.perm;
+    la.first = h->long_first;
+    la.st = h->lst;
+    la.keys = h->lkeys;
+    la.vals = h->lvals;
+    la.old_keys = h->lold_keys;
+    la.old_vals = h->lold_vals;
+    la.old_slots = h->lold_slots;
+    la.active = h->lact;
+    la.nactive = nactive;
+    la.overflow_list = h->lovf;
+    la.overflow_cnt = h->lovf_cnt;
+    la.nnz_row = h->nnz_row;
+    la.mode = mode;
+    CK(h, launch_long(la, h->stream));
+    CK(h, cudaMemcpyAsync(h->pinned + 1, h->lovf_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    s = sync(h);
+    if (s != SPGEMM_SUCCESS) return s;
+    const int64_t novf = *reinterpret_cast<int32_t*>(h->pinned + 1);
+    if (novf == 0) break;
+    // host grows the allocation 2x and relaunches the overflowed rows ([P:297])
+    ++h->growth_rounds;
+    CK(h, launch_long_grow(h->lst, h->lovf, novf, h->lslots, h->lold_slots, h->stream));
+    s = long_alloc_tables(h, h->lovf, novf, fill, true);
+    if (s != SPGEMM_SUCCESS) return s;
+    std::swap(h->lact, h->lovf);
+    nactive = novf;
+  }
+  return SPGEMM_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spgemm_status_string(spgemm_status_t s) {
+  switch (s) {
+    case SPGEMM_SUCCESS: return "SPGEMM_SUCCESS";
+    case SPGEMM_ERROR_INVALID_VALUE: return "SPGEMM_ERROR_INVALID_VALUE";
+    case SPGEMM_ERROR_INVALID_CSR: return "SPGEMM_ERROR_INVALID_CSR";
+    case SPGEMM_ERROR_INDEX_OVERFLOW: return "SPGEMM_ERROR_INDEX_OVERFLOW";
+    case SPGEMM_ERROR_OUT_OF_MEMORY: return "SPGEMM_ERROR_OUT_OF_MEMORY";
+    case SPGEMM_ERROR_INVALID_STATE: return "SPGEMM_ERROR_INVALID_STATE";
+    case SPGEMM_ERROR_CUDA: return "SPGEMM_ERROR_CUDA";
+    case SPGEMM_ERROR_NCCL: return "SPGEMM_ERROR_NCCL";
+    case SPGEMM_ERROR_INTERNAL: return "SPGEMM_ERROR_INTERNAL";
+  }
+  return "SPGEMM_UNKNOWN_STATUS";
+}
+
+const char* spgemm_last_error(spgemm_handle_t h) {
+  if (h && sg_is_dist(h)) return sg_dist_error(h);
+  if (!h) {
+    const char* d = sg_dist_error(nullptr);
+    if (t_last_error.empty() && d && *d) return d;
+  }
+  return h ? h->err.c_str() : t_last_error.c_str();
+}
+
+const char* spgemm_version(void) {
+  return "libspgemm 0.1 (Liu & Vinter four-stage SpGEMM, arXiv 1504.05022) sm_100a";
+}
+
+spgemm_status_t spgemm_set_debug(int32_t force_tier, int64_t long_initial_capacity,
+                                 int64_t long_threshold) {
+  if (force_tier >= NUM_TIERS) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "force_tier out of range");
+  g_force_tier = force_tier;
+  g_long_cap0 = long_initial_capacity > 0 ? long_initial_capacity : 16384;
+  g_long_threshold = long_threshold > 0 ? long_threshold : 0;
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int64_t n,
+                              const int64_t* a_row_ptr, const int32_t* a_col_idx,
+                              const double* a_val, int64_t a_nnz, const int64_t* b_row_ptr,
+                              const int32_t* b_col_idx, const double* b_val, int64_t b_nnz,
+                              spgemm_stream_t stream, uint32_t flags) {
+  if (!handle) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "handle out-pointer is NULL");
+  *handle = nullptr;
+  if (m < 0 || k < 0 || n < 0 || a_nnz < 0 || b_nnz < 0)
+    return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "negative size");
+  if (m > INT32_MAX || k > INT32_MAX || n > INT32_MAX)
+    return fail(nullptr, SPGEMM_ERROR_INDEX_OVERFLOW, "m, k or n exceeds INT32_MAX");
+  const uint32_t known = SPGEMM_FLAG_VALIDATE | SPGEMM_FLAG_INPUTS_REPLICATED | SPGEMM_FLAG_PRECISE |
+                         SPGEMM_FLAG_UPPER_BOUND;
+  if (flags & ~known) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "unknown flag bits 0x%x", flags & ~known);
+  if (!a_row_ptr || !b_row_ptr) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL row_ptr");
+  if ((a_nnz > 0 && (!a_col_idx || !a_val)) || (b_nnz > 0 && (!b_col_idx || !b_val)))
+    return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL col_idx/val with nnz > 0");
+  spgemm_handle_t h = new (std::nothrow) spgemm_handle_s();
+  if (!h) return fail(nullptr, SPGEMM_ERROR_OUT_OF_MEMORY, "host allocation failed");
+  cudaGetDevice(&h->device);
+  h->stream = static_cast<cudaStream_t>(stream);
+  h->flags = flags;
+  h->m = m;
+  h->k = k;
+  h->n = n;
+  h->a_nnz = a_nnz;
+  h->b_nnz = b_nnz;
+  h->A = CsrView{a_row_ptr, a_col_idx, a_val};
+  h->B = CsrView{b_row_ptr, b_col_idx, b_val};
+  // keep freed workspace cached in the stream-ordered pool (warm allocations)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaError_t e = cudaMallocHost(&h->pinned, sizeof(int64_t) * (kSumLen + 8));
+  if (e != cudaSuccess) {
+    spgemm_status_t s = cuda_fail(nullptr, e, "cudaMallocHost");
+    delete h;
+    return s;
+  }
+  for (int i = 0; i < 6; ++i) cudaEventCreate(&h->ev[i]);
+  for (int t = 0; t < NUM_TIERS; ++t)
+    for (int i = 0; i < 2; ++i) cudaEventCreate(&h->tev[t][i]);
+  h->ev_ok = true;
+  if (flags & SPGEMM_FLAG_VALIDATE) {
+    int32_t* err = nullptr;
+    e = cudaMallocAsync(&err, sizeof(int32_t) * 2, h->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int32_t) * 2, h->stream);
+    if (e == cudaSuccess) e = launch_validate(m, k, a_row_ptr, a_col_idx, a_nnz, err, h->stream);
+    if (e == cudaSuccess) e = launch_validate(k, n, b_row_ptr, b_col_idx, b_nnz, err + 1, h->stream);
+    int32_t herr[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(herr, err, sizeof(herr), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (err) cudaFreeAsync(err, h->stream);
+    if (e != cudaSuccess) {
+      spgemm_status_t s = cuda_fail(nullptr, e, "validate");
+      spgemm_destroy(h);
+      return s;
+    }
+    if (herr[0] || herr[1]) {
+      fail(nullptr, SPGEMM_ERROR_INVALID_CSR, "invalid CSR input: A code %d, B code %d", herr[0], herr[1]);
+      spgemm_destroy(h);
+      return SPGEMM_ERROR_INVALID_CSR;
+    }
+  }
+  *handle = h;
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
+  if (!h || !c_nnz) return fail(h, SPGEMM_ERROR_INVALID_VALUE, "NULL handle or c_nnz");
+  cudaSetDevice(h->device);
+  free_symbolic(h);
+  const int64_t m = h->m;
+  const bool precise = (h->flags & SPGEMM_FLAG_PRECISE) != 0;
+  const bool hybrid = !precise;
+  cudaEventRecord(h->ev[0], h->stream);
+  AL(h, &h->c_rp, m + 1);
+  if (m == 0) {
+    CK(h, cudaMemsetAsync(h->c_rp, 0, sizeof(int64_t), h->stream));
+    h->nnz_c = 0;
+    h->sum_u = h->max_u = h->sum_cap = 0;
+    for (int t = 0; t < NUM_TIERS; ++t) h->tier_count[t] = 0;
+    spgemm_status_t s = sync(h);
+    if (s != SPGEMM_SUCCESS) return s;
+    h->sym_ok = true;
+    *c_nnz = 0;
+    return SPGEMM_SUCCESS;
+  }
+  Stage12Ws& ws = h->ws;
+  ws.nblk = (m + kS12RowsPerBlock - 1) / kS12RowsPerBlock;
+  AL(h, &ws.U, m);
+  AL(h, &ws.tier, m);
+  AL(h, &ws.perm, m);
+  AL(h, &ws.ctil_off, m + 1);
+  AL(h, &ws.blk_tier, ws.nblk * NUM_TIERS);
+  AL(h, &ws.blk_cap, ws.nblk);
+  AL(h, &ws.blk_usum, ws.nblk);
+  AL(h, &ws.blk_umax, ws.nblk);
+  AL(h, &ws.summary, kSumLen);
+  AL(h, &h->nnz_row, m);
+  AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
+  // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
+  CK(h, cudaMemsetAsync(h->nnz_row, 0, sizeof(int64_t) * m, h->stream));
+  TierParams tp{g_force_tier, g_long_threshold};
+  tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
+  for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = false;
+  CK(h, launch_stage1(m, h->n, h->A, h->B.rp, tp, hybrid, ws, h->stream));
+  CK(h, launch_stage2(m, ws, hybrid, h->n, h->stream));
+  h->launches_sym = 3;
+  CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
+  spgemm_status_t s = sync(h);
+  if (s != SPGEMM_SUCCESS) return s;
+  for (int t = 0; t < NUM_TIERS; ++t) {
+    h->tier_count[t] = h->pinned[kSumCount + t];
+    h->tier_off[t] = h->pinned[kSumOff + t];
+  }
+  h->tier_off[NUM_TIERS] = h->pinned[kSumOff + NUM_TIERS];
+  h->sum_u = h->pinned[kSumU];
+  h->sum_cap = h->pinned[kSumCap];
+  h->max_u = h->pinned[kSumUMax];
+  if (hybrid) {
+    AL(h, &h->ctil_col, h->sum_cap);
+    AL(h, &h->ctil_val, h->sum_cap);
+  }
+  cudaEventRecord(h->ev[1], h->stream);
+  // stage 3: one launch per non-empty class ([P:264] "only issue kernels for non-empty bins")
+  for (int t = T_G1; t <= T_C8192; ++t) {
+    if (h->tier_count[t] == 0) continue;
+    Stage3Args a{};
+    a.A = h->A;
+    a.B = h->B;
+    a.n = h->n;
+    a.perm = ws.perm;
+    a.first = h->tier_off[t];
+    a.count = h->tier_count[t];
+    a.out_off = ws.ctil_off;
+    a.out_col = h->ctil_col;
+    a.out_val = h->ctil_val;
+    a.nnz_row = h->nnz_row;
+    a.mode = hybrid ? MODE_FILL : MODE_COUNT;
+    cudaEventRecord(h->tev[t][0], h->stream);
+    CK(h, launch_stage3_tier(t, a, h->stream));
+    cudaEventRecord(h->tev[t][1], h->stream);
+    h->tev_used[t] = true;
+    ++h->launches_sym;
+  }
+  h->nlong = h->tier_count[T_LONG];
+  h->long_first = h->tier_off[T_LONG];
+  if (h->nlong > 0) cudaEventRecord(h->tev[T_LONG][0], h->stream);
+  s = run_long(h, hybrid ? MODE_FILL : MODE_COUNT);
+  if (s != SPGEMM_SUCCESS) return s;
+  if (h->nlong > 0) {
+    cudaEventRecord(h->tev[T_LONG][1], h->stream);
+    h->tev_used[T_LONG] = true;
+    h->launches_sym += 4 + 6 * h->growth_rounds;
+  }
+  if (precise && h->nlong > 0) {
+    // exact tables for numeric (no growth: cap = nnz(c_i*)); allocated now so numeric never syncs
+    const unsigned g = (unsigned)((h->nlong + 255) / 256);
+    k_long_exact<<<g, 256, 0, h->stream>>>(h->lst, ws.perm, h->long_first, h->nlong, h->nnz_row,
+                                           h->A.rp, h->lslots);
+    CK(h, cudaGetLastError());
+    h->long_entries = 0;
+    s = long_alloc_tables(h, h->liota, h->nlong, true, false);
+    if (s != SPGEMM_SUCCESS) return s;
+    CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * h->nlong, h->stream));
+  }
+  cudaEventRecord(h->ev[2], h->stream);
+  // stage 4 (first half): sum the numbers of nonzero entries of all rows [P:301]
+  CK(h, launch_exclusive_scan(h->nnz_row, h->c_rp, m, h->scan_tmp, h->stream));
+  h->launches_sym += 3;
+  if (precise && h->nlong > 0) h->launches_sym += 4;
+  cudaEventRecord(h->ev[3], h->stream);
+  CK(h, cudaMemcpyAsync(h->pinned, h->c_rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  s = sync(h);
+  if (s != SPGEMM_SUCCESS) return s;
+  h->nnz_c = h->pinned[0];
+  h->sym_ok = true;
+  *c_nnz = h->nnz_c;
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c_col_idx,
+                               double* c_val) {
+  if (!h) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL handle");
+  if (!h->sym_ok) return fail(h, SPGEMM_ERROR_INVALID_STATE, "numeric before a successful symbolic");
+  if (!c_row_ptr || (h->nnz_c > 0 && (!c_col_idx || !c_val)))
+    return fail(h, SPGEMM_ERROR_INVALID_VALUE, "NULL output pointer");
+  cudaSetDevice(h->device);
+  cudaEventRecord(h->ev[4], h->stream);
+  h->launches_num = 0;
+  CK(h, cudaMemcpyAsync(c_row_ptr, h->c_rp, sizeof(int64_t) * (h->m + 1), cudaMemcpyDeviceToDevice, h->stream));
+  if (h->m > 0 && h->nnz_c > 0) {
+    const bool precise = (h->flags & SPGEMM_FLAG_PRECISE) != 0;
+    CopyArgs ca{};
+    ca.m = h->m;
+    ca.perm = h->ws.perm;
+    ca.long_first = h->long_first;
+    ca.nlong = h->nlong;
+    ca.c_rp = h->c_rp;
+    ca.ctil_off = h->ws.ctil_off;
+    ca.tier = h->ws.tier;
+    ca.ctil_col = h->ctil_col;
+    ca.ctil_val = h->ctil_val;
+    ca.long_keys = h->lkeys;
+    ca.long_vals = h->lvals;
+    ca.c_col = c_col_idx;
+    ca.c_val = c_val;
+    if (precise) {
+      // stage 3 again, values on, straight into C at its final offsets
+      for (int t = T_G1; t <= T_C8192; ++t) {
+        if (h->tier_count[t] == 0) continue;
+        Stage3Args a{};
+        a.A = h->A;
+        a.B = h->B;
+        a.n = h->n;
+        a.perm = h->ws.perm;
+        a.first = h->tier_off[t];
+        a.count = h->tier_count[t];
+        a.out_off = h->c_rp;
+        a.out_col = c_col_idx;
+        a.out_val = c_val;
+        a.nnz_row = nullptr;
+        a.mode = MODE_FILL;
+        cudaEventRecord(h->tev[t][0], h->stream);
+        CK(h, launch_stage3_tier(t, a, h->stream));
+        cudaEventRecord(h->tev[t][1], h->stream);
+        h->tev_used[t] = true;
+        ++h->launches_num;
+      }
+      if (h->nlong > 0) {
+        LongArgs la{};
+        la.A = h->A;
+        la.B = h->B;
+        la.n = h->n;
+        la.perm = h->ws.perm;
+        la.first = h->long_first;
+        la.st = h->lst;
+        la.keys = h->lkeys;
+        la.vals = h->lvals;
+        la.old_keys = nullptr;
+        la.active = h->liota;
+        la.nactive = h->nlong;
+        la.overflow_list = h->lovf;
+        la.overflow_cnt = h->lovf_cnt;
+        la.nnz_row = nullptr;
+        la.mode = MODE_FILL;
+        cudaEventRecord(h->tev[T_LONG][0], h->stream);
+        CK(h, launch_long(la, h->stream));
+        cudaEventRecord(h->tev[T_LONG][1], h->stream);
+        h->tev_used[T_LONG] = true;
+        ++h->launches_num;
+      }
+      ca.m = 0;  // only the long rows are copied
+    }
+    const double avg = double(h->nnz_c) / double(h->m);
+    const int group = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    CK(h, launch_copy(ca, group, h->stream));
+    h->launches_num += (ca.m > 0 ? 1 : 0) + (ca.nlong > 0 ? 1 : 0);
+  }
+  cudaEventRecord(h->ev[5], h->stream);
+  h->numeric_recorded = true;
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_destroy(spgemm_handle_t h) {
+  if (!h) return SPGEMM_SUCCESS;
+  if (sg_is_dist(h)) return sg_dist_destroy(h);
+  cudaSetDevice(h->device);
+  free_symbolic(h);
+  cudaStreamSynchronize(h->stream);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->ev_ok) {
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(h->ev[i]);
+    for (int t = 0; t < NUM_TIERS; ++t)
+      for (int i = 0; i < 2; ++i) cudaEventDestroy(h->tev[t][i]);
+  }
+  delete h;
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_get_stats(spgemm_handle_t h, spgemm_stats_t* out) {
+  if (!h || !out) return fail(h, SPGEMM_ERROR_INVALID_VALUE, "NULL handle or out");
+  if (sg_is_dist(h)) return sg_dist_stats(h, out);
+  memset(out, 0, sizeof(*out));
+  out->m = h->m;
+  out->k = h->k;
+  out->n = h->n;
+  out->nnz_a = h->a_nnz;
+  out->nnz_b = h->b_nnz;
+  out->sum_u = h->sum_u;
+  out->nnz_c = h->nnz_c;
+  out->max_u = h->max_u;
+  for (int t = 0; t < NUM_TIERS; ++t) out->tier_rows[t] = h->tier_count[t];
+  out->ctil_entries = (h->flags & SPGEMM_FLAG_PRECISE) ? 0 : h->sum_cap;
+  out->long_rows = h->nlong;
+  out->long_entries = h->long_entries;
+  out->growth_rounds = h->growth_rounds;
+  out->flags = (int32_t)h->flags;
+  out->workspace_bytes = (int64_t)h->bytes;
+  if (h->sym_ok && h->ev_ok) {
+    cudaEventSynchronize(h->ev[3]);
+    cudaEventElapsedTime(&out->stage_ms[0], h->ev[0], h->ev[1]);
+    cudaEventElapsedTime(&out->stage_ms[1], h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&out->stage_ms[2], h->ev[2], h->ev[3]);
+    if (h->numeric_recorded) {
+      cudaEventSynchronize(h->ev[5]);
+      cudaEventElapsedTime(&out->stage_ms[3], h->ev[4], h->ev[5]);
+    }
+    for (int t = 0; t < NUM_TIERS; ++t)
+      if (h->tev_used[t]) {
+        cudaEventSynchronize(h->tev[t][1]);
+        cudaEventElapsedTime(&out->tier_ms[t], h->tev[t][0], h->tev[t][1]);
+      }
+    out->launches_symbolic = h->launches_sym;
+    out->launches_numeric = h->launches_num;
+    if (h->m > 0) {
+      unsigned long long* d = nullptr;
+      std::vector<unsigned long long> hs(3 * NUM_TIERS);
+      CK(h, cudaMallocAsync(&d, sizeof(unsigned long long) * 3 * NUM_TIERS, h->stream));
+      CK(h, cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 3 * NUM_TIERS, h->stream));
+      k_class_sums<<<256, 256, 0, h->stream>>>(h->m, h->ws.tier, h->ws.U, h->A.rp, h->nnz_row, d);
+      CK(h, cudaGetLastError());
+      CK(h, cudaMemcpyAsync(hs.data(), d, sizeof(unsigned long long) * 3 * NUM_TIERS, cudaMemcpyDeviceToHost,
+                            h->stream));
+      CK(h, cudaFreeAsync(d, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
+      for (int t = 0; t < NUM_TIERS; ++t) {
+        out->tier_a_entries[t] = (int64_t)hs[t];
+        out->tier_products[t] = (int64_t)hs[NUM_TIERS + t];
+        out->tier_c_entries[t] = (int64_t)hs[2 * NUM_TIERS + t];
+      }
+    }
+  }
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_debug_get_u(spgemm_handle_t h, int64_t* u, int32_t* tier) {
+  if (!h || !u) return fail(h, SPGEMM_ERROR_INVALID_VALUE, "NULL handle or u");
+  if (!h->sym_ok) return fail(h, SPGEMM_ERROR_INVALID_STATE, "no symbolic yet");
+  if (h->m == 0) return SPGEMM_SUCCESS;
+  CK(h, cudaMemcpyAsync(u, h->ws.U, sizeof(int64_t) * h->m, cudaMemcpyDeviceToDevice, h->stream));
+  if (tier) {
+    k_tier_to_i32<<<(unsigned)((h->m + 255) / 256), 256, 0, h->stream>>>(h->ws.tier, tier, h->m);
+    CK(h, cudaGetLastError());
+  }
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_partition_rows(const int64_t* scan, int64_t m, int nranks, int64_t* splits) {
+  if (!splits || nranks < 1 || m < 0 || (m > 0 && !scan))
+    return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "bad partition arguments");
+  const int64_t total = m > 0 ? scan[m - 1] : 0;
+  splits[0] = 0;
+  for (int r = 1; r < nranks; ++r) {
+    // s_r = min{ i : scan[i] >= ceil(r·total/P) }, as a row count (rows [0, s_r] go left)
+    const __int128 num = (__int128)r * total;
+    const int64_t target = (int64_t)((num + nranks - 1) / nranks);
+    int64_t lo = 0, hi = m;  // first index with scan[idx] >= target
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (scan[mid] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    int64_t s = lo < m ? lo + 1 : m;
+    if (target == 0) s = 0;
+    if (s < splits[r - 1]) s = splits[r - 1];
+    splits[r] = s;
+  }
+  splits[nranks] = m;
+  return SPGEMM_SUCCESS;
+}
+
+}  // extern "C"

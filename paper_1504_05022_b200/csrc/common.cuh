@@ -1,0 +1,193 @@
+// common.cuh — internal declarations of libspgemm (CUDA, sm_100a).  Not part of the ABI.
+//
+// Stage-2 size classes ("tiers") re-derived for B200.  The paper bins rows
+// by the stage-1 bound u_i into 38 bins / 5 groups sized for 48-96 KB scratchpads
+// ([P:214-260], [P:299] "the parameters of the binning depends on specifications ... of GPU
+// architectures").  Here, with cap_i = min(u_i, n) >= nnz(c_i*):
+//   T_EMPTY            u = 0                      nothing to compute ([P:216])
+//   T_G1..T_G32        u <= G (G = 1..32)         G-lane group per row, products sorted in
+//                                                 registers (slot of the paper's heap group 3)
+//   T_W64..T_W2048     1.25·cap <= S              one warp per row, S-slot shared-memory hash
+//                                                 (slot of the bitonic-ESC group 4)
+//   T_C2048..T_C8192   cap <= H                   one CTA per row, order-preserving hash with
+//                                                 H home slots in 2H smem slots
+//   T_LONG             otherwise                  progressive global table + re-allocation
+//                                                 (group 5, [P:286-297])
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spgemm.h"
+
+namespace sg {
+
+enum Tier : int {
+  T_EMPTY = 0,
+  T_G1 = 1, T_G2 = 2, T_G4 = 3, T_G8 = 4, T_G16 = 5, T_G32 = 6,
+  T_W64 = 7, T_W128 = 8, T_W256 = 9, T_W512 = 10, T_W1024 = 11, T_W2048 = 12,
+  T_C2048 = 13, T_C4096 = 14, T_C8192 = 15,
+  T_LONG = 16,
+  NUM_TIERS = 17
+};
+static_assert(NUM_TIERS == SPGEMM_NUM_TIERS, "tier count mismatch with the ABI header");
+
+constexpr int kEmptyKey = -1;
+
+struct TierParams {
+  int force_tier;         // -1 = off
+  int64_t long_threshold; // rows with cap above go long (0 = default by smem)
+};
+
+__host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap) {
+  if (t == T_EMPTY) return u == 0;
+  if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
+  if (t >= T_W64 && t <= T_W2048) {
+    int64_t S = int64_t(64) << (t - T_W64);
+    return 4 * S >= 5 * cap;
+  }
+  if (t >= T_C2048 && t <= T_C8192) return cap <= (int64_t(2048) << (t - T_C2048));
+  return 1;  // T_LONG holds anything
+}
+
+// Stage-2 classification of one row (the B200 re-derivation of Algorithm 3 [P:226-260]).
+__host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
+  if (u == 0) return T_EMPTY;
+  int64_t cap = u < n ? u : n;
+  if (p.force_tier >= 0 && u >= 2 && tier_capacity_ok(p.force_tier, u, cap)) return p.force_tier;
+  if (p.long_threshold > 0 && cap > p.long_threshold) return T_LONG;
+  if (u <= 32) {
+    int g = 0;
+    while ((int64_t(1) << g) < u) ++g;
+    return T_G1 + g;
+  }
+  for (int t = T_W64; t <= T_C8192; ++t)
+    if (tier_capacity_ok(t, u, cap)) return t;
+  return T_LONG;
+}
+
+// Hybrid C~ capacity of a row ([P:224]: u_i for short rows; here min(u_i, n) which is
+// still a safe bound since nnz(c_i*) <= n).  Long rows live in their own growing arena.
+__host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n) {
+  if (t == T_LONG) return 0;
+  return u < n ? u : n;
+}
+
+struct CsrView {
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* val;
+};
+
+enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1 };
+
+struct Stage3Args {
+  CsrView A, B;
+  int64_t n;
+  const int32_t* perm;   // rows grouped by tier
+  int64_t first;         // this tier's rows are perm[first, first + count)
+  int64_t count;
+  const int64_t* out_off;  // per-row output offset (C~ offsets or C row_ptr), by row id
+  int32_t* out_col;
+  double* out_val;
+  int64_t* nnz_row;        // per-row nnz (written in both modes; may be NULL in numeric)
+  int mode;
+};
+
+// ---- host-side launchers (defined in the .cu files) --------------------------------
+struct Stage12Ws {
+  int64_t* U;          // [m]
+  uint8_t* tier;       // [m]
+  int32_t* perm;       // [m]
+  int64_t* ctil_off;   // [m+1]
+  int32_t* blk_tier;   // [nblk * NUM_TIERS]
+  int64_t* blk_cap;    // [nblk]
+  int64_t* blk_usum;   // [nblk]
+  int64_t* blk_umax;   // [nblk]
+  int64_t* summary;    // [NUM_TIERS (counts) + NUM_TIERS+1 (offsets) + 3] device
+  int64_t nblk;
+};
+constexpr int kS12Threads = 256;
+constexpr int kS12RowsPerThread = 8;
+constexpr int64_t kS12RowsPerBlock = int64_t(kS12Threads) * kS12RowsPerThread;
+// summary layout
+constexpr int kSumCount = 0;                       // tier counts [NUM_TIERS]
+constexpr int kSumOff = NUM_TIERS;                 // tier offsets [NUM_TIERS+1]
+constexpr int kSumU = 2 * NUM_TIERS + 1;           // sum u
+constexpr int kSumCap = kSumU + 1;                 // sum cap (C~ entries)
+constexpr int kSumUMax = kSumU + 2;                // max u
+constexpr int kSumLen = kSumU + 3;
+
+cudaError_t launch_stage1(int64_t m, int64_t n, CsrView A, const int64_t* b_rp, TierParams tp,
+                          bool hybrid_caps, Stage12Ws& ws, cudaStream_t s);
+cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n, cudaStream_t s);
+
+cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
+
+// Exclusive scan of int64 values x[0..len) into y[0..len]; y[len] = total.  tmp must hold
+// scan_tmp_elems(len) int64.
+int64_t scan_tmp_elems(int64_t len);
+cudaError_t launch_exclusive_scan(const int64_t* x, int64_t* y, int64_t len, int64_t* tmp,
+                                  cudaStream_t s);
+
+// Long-row (T_LONG) progressive path --------------------------------------------------
+struct LongState {
+  int64_t next_a;   // checkpoint: index of the next unprocessed a_ij ([P:297])
+  int64_t cap;      // current capacity in entries (table has 2*cap slots)
+  int64_t capmax;   // min(u_i, n)
+  int64_t count;    // distinct keys so far
+  int32_t lo, hi;   // column window of the row
+  int32_t done;
+  int32_t pad;
+};
+struct LongArgs {
+  CsrView A, B;
+  int64_t n;
+  const int32_t* perm;
+  int64_t first;          // perm index of long row 0
+  LongState* st;          // [nlong]
+  int32_t** keys;         // [nlong] table pointers (current)
+  double** vals;
+  int32_t** old_keys;     // [nlong] previous tables (reload on growth), may hold NULL
+  double** old_vals;
+  int64_t* old_slots;     // [nlong]
+  const int32_t* active;  // list of long-row indices to run
+  int64_t nactive;
+  int32_t* overflow_list; // out: overflowed long-row indices
+  int32_t* overflow_cnt;  // out: count
+  int64_t* nnz_row;       // by row id
+  int mode;
+};
+cudaError_t launch_long_init(LongState* st, const int32_t* perm, int64_t first, int64_t nlong,
+                             const int64_t* U, int64_t n, int64_t cap0, CsrView A, CsrView B,
+                             cudaStream_t s);
+cudaError_t launch_long(const LongArgs& a, cudaStream_t s);
+// After an overflow: new cap = min(2*cap, capmax) for rows in `list`; writes slots needed
+// (2*cap) per listed row into slots_out[i].
+cudaError_t launch_long_grow(LongState* st, const int32_t* list, int64_t nlist,
+                             int64_t* slots_out, int64_t* old_slots, cudaStream_t s);
+cudaError_t launch_long_assign(const int32_t* list, int64_t nlist, const int64_t* slot_off,
+                               int32_t* keys_base, double* vals_base, int32_t** keys,
+                               double** vals, int32_t** old_keys, double** old_vals,
+                               int64_t* old_slots, const LongState* st, cudaStream_t s);
+
+// Stage 4 -------------------------------------------------------------------------------
+struct CopyArgs {
+  int64_t m;
+  const int32_t* perm;       // long rows are perm[long_first, long_first + nlong)
+  int64_t long_first, nlong;
+  const int64_t* c_rp;       // final row pointers [m+1]
+  const int64_t* ctil_off;   // by row (C~ offsets; unused for long rows)
+  const uint8_t* tier;
+  const int32_t* ctil_col;
+  const double* ctil_val;
+  int32_t* const* long_keys;
+  double* const* long_vals;
+  int32_t* c_col;
+  double* c_val;
+};
+cudaError_t launch_copy(const CopyArgs& a, int group, cudaStream_t s);
+
+cudaError_t launch_validate(int64_t rows, int64_t cols, const int64_t* rp, const int32_t* ci,
+                            int64_t nnz, int32_t* err, cudaStream_t s);
+
+}  // namespace sg

@@ -1,0 +1,487 @@
+// stage3.cu — stage 3 ("computing the resulting matrix", [P:262-284]) for rows whose
+// products fit on chip.  Each kernel computes, for a row i, the sorted duplicate-free set
+// {k : exists j, a_ij and b_jk stored} and c_ik = sum_j a_ij·b_jk — Algorithm "Pseudocode
+// for the SpGEMM" lines 3-11 [P:121-135]: per product an "insert" (new column) or an
+// "accumulate" (existing column).
+//
+// The paper's group-3 heap [P:266-275] and group-4 bitonic ESC [P:277-284] were sized for
+// 48-96 KB scratchpads and 32-wide thread bunches; on B200 they become:
+//   k_group<G>   u_i <= G <= 32: G lanes per row, lane = one product; the products are
+//                sorted by (column, product index) with a register bitonic network and
+//                fused left to right — the ESC idea with the whole row in registers.
+//   k_warp_hash  one warp per row, S-slot shared-memory hash; lanes walk one row b_j* at a
+//                time (columns within a row of B are distinct, so no two lanes of one
+//                instruction touch one slot); accumulation order per column = j ascending.
+//                Then compaction + shared-memory bitonic sort (the paper's ESC sort step).
+//   k_cta_hash   one CTA per row, order-preserving hash (home slot monotone in the column)
+//                with linear probing into 2H slots: clusters come out ordered, only each
+//                cluster is insertion-sorted before the ordered compaction.
+// Values: products are rounded separately (__dmul_rn, no FMA) and summed with __dadd_rn.
+// k_group and k_warp_hash add in j-ascending order starting from the first product (the
+// warp hash starts from -0.0, the identity of +), i.e. the oracle's order [P:129-131].
+#include <climits>
+
+#include "common.cuh"
+
+namespace sg {
+
+namespace {
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// --------------------------------------------------------------- G-lane sort groups
+template <int G, int NT>
+__global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
+  static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
+  __shared__ int s_col[NT];
+  __shared__ double s_val[NT];
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gfirst = threadIdx.x & ~(G - 1);
+  const int gshift = lane & ~(G - 1);
+  const unsigned gbits = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gshift);
+  const int warp = threadIdx.x >> 5;
+  constexpr int WPB = NT / 32;
+  constexpr int GPW = 32 / G;
+  const bool fill = a.mode == MODE_FILL;
+
+  for (int64_t wt = int64_t(blockIdx.x) * WPB + warp; wt * GPW < a.count;
+       wt += int64_t(gridDim.x) * WPB) {
+    const int64_t gi = wt * GPW + lane / G;
+    const bool has = gi < a.count;
+    const int row = has ? __ldg(a.perm + a.first + gi) : 0;
+    const int64_t a0 = has ? __ldg(a.A.rp + row) : 0;
+    const int64_t a1 = has ? __ldg(a.A.rp + row + 1) : 0;
+    int64_t maxlen = a1 - a0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
+      maxlen = x > maxlen ? x : maxlen;
+    }
+    int cnt = 0;  // products gathered so far in this group
+    unsigned long long key = ~0ull;
+    double myv = 0.0;
+    for (int64_t e0 = 0; e0 < maxlen; e0 += G) {
+      const int64_t e = a0 + e0 + gl;
+      int len = 0;
+      int64_t bs = 0;
+      double av = 0.0;
+      if (e < a1) {
+        const int j = __ldg(a.A.ci + e);
+        if (fill) av = __ldg(a.A.val + e);
+        bs = __ldg(a.B.rp + j);
+        len = (int)(__ldg(a.B.rp + j + 1) - bs);
+      }
+      int inc = len;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, inc, o, G);
+        if (gl >= o) inc += x;
+      }
+      const int tot = __shfl_sync(0xffffffffu, inc, G - 1, G);
+      const int q = gl - cnt;  // product index (within this chunk) this lane receives
+      int lo = 0;
+#pragma unroll
+      for (int step = G / 2; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, inc, lo + step - 1, G);
+        if (v <= q) lo += step;
+      }
+      const int64_t obs = __shfl_sync(0xffffffffu, bs, lo, G);
+      const double oa = __shfl_sync(0xffffffffu, av, lo, G);
+      const int oex = __shfl_sync(0xffffffffu, inc - len, lo, G);
+      if (q >= 0 && q < tot) {
+        const int64_t qq = obs + (q - oex);
+        const int c = __ldg(a.B.ci + qq);
+        key = ((unsigned long long)(unsigned)c << 32) | (unsigned)gl;
+        if (fill) myv = __dmul_rn(oa, __ldg(a.B.val + qq));   // line 6: value <- a_ij b_jk
+      }
+      cnt += tot;
+    }
+    // bitonic sort of (column, product index) across the G lanes of the group
+#pragma unroll
+    for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const unsigned long long p = __shfl_xor_sync(0xffffffffu, key, j);
+        const bool up = (gl & k) == 0, lower = (gl & j) == 0;
+        key = (lower == up) ? (key < p ? key : p) : (key > p ? key : p);
+      }
+    }
+    const bool valid = key != ~0ull;
+    const int col = valid ? (int)(key >> 32) : -1;
+    const int src = (int)(key & 31u);
+    const double v = __shfl_sync(0xffffffffu, myv, valid ? src : gl, G);
+    const int prev = __shfl_up_sync(0xffffffffu, col, 1, G);
+    const bool head = valid && (gl == 0 || prev != col);
+    const unsigned hb = __ballot_sync(0xffffffffu, head) & gbits;
+    const int nnz = __popc(hb);
+    if (has && gl == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    if (fill) {
+      s_col[threadIdx.x] = col;
+      s_val[threadIdx.x] = v;
+      __syncwarp();
+      if (has && head) {
+        double acc = v;                                    // line 9: c_ik <- value
+        for (int t = gl + 1; t < G && s_col[gfirst + t] == col; ++t)
+          acc = __dadd_rn(acc, s_val[gfirst + t]);         // line 11: c_ik += value
+        const int pos = __popc(hb & lanemask_lt());
+        const int64_t o = __ldg(a.out_off + row) + pos;
+        a.out_col[o] = col;
+        a.out_val[o] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// --------------------------------------------------------------- warp hash (T_W*)
+__device__ __forceinline__ int ht_insert(int* keys, int c, unsigned mask, int shift, int& isnew) {
+  unsigned h = ((unsigned)c * 0x9E3779B1u) >> shift;
+  volatile int* vk = keys;
+  while (true) {
+    const int k = vk[h];
+    if (k == c) {
+      isnew = 0;
+      return (int)h;
+    }
+    if (k == kEmptyKey) {
+      const int old = atomicCAS(&keys[h], kEmptyKey, c);
+      if (old == kEmptyKey) {
+        isnew = 1;
+        return (int)h;
+      }
+      if (old == c) {
+        isnew = 0;
+        return (int)h;
+      }
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+template <int LOG2S, int NW>
+__global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
+  constexpr int S = 1 << LOG2S;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool fill = a.mode == MODE_FILL;
+  int* keys = reinterpret_cast<int*>(smem) + w * S;
+  double* vals = reinterpret_cast<double*>(smem + size_t(NW) * S * sizeof(int)) + w * S;
+
+  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+    const int row = __ldg(a.perm + a.first + r);
+    for (int s = lane; s < S; s += 32) {
+      keys[s] = kEmptyKey;
+      if (fill) vals[s] = -0.0;  // -0.0 + x == x for every x: first add == "c_ik <- value"
+    }
+    __syncwarp();
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int inserted = 0;
+    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+      const int64_t e = e0 + lane;
+      int64_t bs = 0, be = 0;
+      double av = 0.0;
+      if (e < a1) {
+        const int j = __ldg(a.A.ci + e);
+        if (fill) av = __ldg(a.A.val + e);
+        bs = __ldg(a.B.rp + j);
+        be = __ldg(a.B.rp + j + 1);
+      }
+      const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+      for (int t = 0; t < nE; ++t) {
+        const int64_t jb = __shfl_sync(0xffffffffu, bs, t);
+        const int64_t je = __shfl_sync(0xffffffffu, be, t);
+        const double at = __shfl_sync(0xffffffffu, av, t);
+        for (int64_t q0 = jb; q0 < je; q0 += 32) {
+          const int64_t q = q0 + lane;
+          const bool act = q < je;
+          int slot = 0;
+          double v = 0.0;
+          if (act) {
+            const int c = __ldg(a.B.ci + q);
+            if (fill) v = __dmul_rn(at, __ldg(a.B.val + q));
+            int isnew;
+            slot = ht_insert(keys, c, S - 1, 32 - LOG2S, isnew);
+            inserted += isnew;
+          }
+          if (fill) {
+            __syncwarp();
+            if (act) vals[slot] = __dadd_rn(vals[slot], v);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (!fill) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = inserted;
+      continue;
+    }
+    // ordered compaction of occupied slots to the front
+    int cnt = 0;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+      const int s = s0 + lane;
+      const int k = keys[s];
+      const double v = vals[s];
+      const bool occ = k != kEmptyKey;
+      const unsigned bal = __ballot_sync(0xffffffffu, occ);
+      const int pos = cnt + __popc(bal & lanemask_lt());
+      __syncwarp();
+      if (occ) {
+        keys[pos] = k;
+        vals[pos] = v;
+      }
+      cnt += __popc(bal);
+      __syncwarp();
+    }
+    int N = 1;
+    while (N < cnt) N <<= 1;
+    for (int s = cnt + lane; s < N; s += 32) keys[s] = INT_MAX;
+    __syncwarp();
+    // bitonic sort of (key, value) in shared memory (the ESC sort, [P:277-284])
+    for (int k = 2; k <= N; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < (N >> 1); i += 32) {
+          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          const int hi = lo + j;
+          const bool asc = (lo & k) == 0;
+          const int kl = keys[lo], kh = keys[hi];
+          if ((kl > kh) == asc) {
+            keys[lo] = kh;
+            keys[hi] = kl;
+            const double t = vals[lo];
+            vals[lo] = vals[hi];
+            vals[hi] = t;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    const int64_t o = __ldg(a.out_off + row);
+    for (int t = lane; t < cnt; t += 32) {
+      a.out_col[o + t] = keys[t];
+      a.out_val[o + t] = vals[t];
+    }
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------------- CTA order-preserving hash
+template <int NT>
+__device__ __forceinline__ int block_excl_scan_int(int v, int* total, int* s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int x = lane < NT / 32 ? s_w[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    if (lane < NT / 32) s_w[lane] = xi - x;
+    if (lane == 31) s_w[NT / 32] = xi;
+  }
+  __syncthreads();
+  const int ex = inc - v + s_w[w];
+  *total = s_w[NT / 32];
+  __syncthreads();
+  return ex;
+}
+
+template <int LOG2H, int NT>
+__global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
+  constexpr int H = 1 << LOG2H;
+  constexpr int S = 2 * H;  // physical slots: probes never wrap (nnz <= cap <= H)
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int* keys = reinterpret_cast<int*>(smem);
+  double* vals = reinterpret_cast<double*>(smem + size_t(S) * sizeof(int));
+  __shared__ int s_w[NW + 1];
+  __shared__ int s_lo[NW], s_hi[NW];
+  __shared__ int s_cnt;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool fill = a.mode == MODE_FILL;
+
+  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    // column window [lo, hi] of the row: first/last column of each b_j*
+    int lo = INT_MAX, hi = -1;
+    for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
+      const int j = __ldg(a.A.ci + e);
+      const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
+      if (be > bs) {
+        lo = min(lo, __ldg(a.B.ci + bs));
+        hi = max(hi, __ldg(a.B.ci + be - 1));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      s_lo[w] = lo;
+      s_hi[w] = hi;
+    }
+    for (int s = threadIdx.x; s < S; s += NT) {
+      keys[s] = kEmptyKey;
+      if (fill) vals[s] = 0.0;
+    }
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    lo = s_lo[0];
+    hi = s_hi[0];
+    for (int k = 1; k < NW; ++k) {
+      lo = min(lo, s_lo[k]);
+      hi = max(hi, s_hi[k]);
+    }
+    const int64_t W = int64_t(hi) - lo + 1;
+    const float scale = W <= H ? 1.0f : (float)H / (float)W;
+    int inserted = 0;
+    for (int64_t e = a0 + w; e < a1; e += NW) {
+      const int j = __ldg(a.A.ci + e);
+      const double at = fill ? __ldg(a.A.val + e) : 0.0;
+      const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
+      for (int64_t q = jb + lane; q < je; q += 32) {
+        const int c = __ldg(a.B.ci + q);
+        int h = (int)__fmul_rz((float)(c - lo), scale);   // monotone in c
+        h = h < H - 1 ? h : H - 1;
+        volatile int* vk = keys;
+        while (true) {
+          const int k = vk[h];
+          if (k == c) break;
+          if (k == kEmptyKey) {
+            const int old = atomicCAS(&keys[h], kEmptyKey, c);
+            if (old == kEmptyKey) {
+              ++inserted;
+              break;
+            }
+            if (old == c) break;
+          }
+          ++h;
+        }
+        if (fill) atomicAdd(&vals[h], __dmul_rn(at, __ldg(a.B.val + q)));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+    if (lane == 0) atomicAdd(&s_cnt, inserted);
+    __syncthreads();
+    const int nnz = s_cnt;
+    if (!fill) {
+      if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+      __syncthreads();
+      continue;
+    }
+    // order each cluster (maximal run of occupied slots) by insertion sort
+    constexpr int CH = S / NT;
+    for (int s = threadIdx.x * CH; s < (threadIdx.x + 1) * CH; ++s) {
+      if (keys[s] == kEmptyKey || (s > 0 && keys[s - 1] != kEmptyKey)) continue;
+      int end = s + 1;
+      while (end < S && keys[end] != kEmptyKey) ++end;
+      for (int x = s + 1; x < end; ++x) {
+        const int kx = keys[x];
+        const double vx = vals[x];
+        int y = x - 1;
+        while (y >= s && keys[y] > kx) {
+          keys[y + 1] = keys[y];
+          vals[y + 1] = vals[y];
+          --y;
+        }
+        keys[y + 1] = kx;
+        vals[y + 1] = vx;
+      }
+    }
+    __syncthreads();
+    const int64_t o = __ldg(a.out_off + row);
+    int base = 0;
+    for (int s0 = 0; s0 < S; s0 += NT) {
+      const int s = s0 + threadIdx.x;
+      const bool occ = keys[s] != kEmptyKey;
+      int tot;
+      const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);
+      if (occ) {
+        a.out_col[o + base + pos] = keys[s];
+        a.out_val[o + base + pos] = vals[s];
+      }
+      base += tot;
+    }
+    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------- launch helpers
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename K>
+cudaError_t launch_persistent(K kernel, int nt, size_t dsmem, int64_t work_units, int units_per_block,
+                              const Stage3Args& a, cudaStream_t s) {
+  if (dsmem > 0) {  // opt in whenever static + dynamic may exceed the 48 KB default
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+    if (e != cudaSuccess) return e;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, dsmem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t need = (work_units + units_per_block - 1) / units_per_block;
+  int64_t cap = int64_t(num_sms()) * per_sm * 8;
+  int64_t grid = need < cap ? need : cap;
+  if (grid < 1) grid = 1;
+  kernel<<<(unsigned)grid, nt, dsmem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const bool fill = a.mode == MODE_FILL;
+  const size_t per_slot = fill ? 12 : 4;
+  switch (tier) {
+    case T_G1: return launch_persistent(k_group<1, 256>, 256, 0, a.count, 256, a, s);
+    case T_G2: return launch_persistent(k_group<2, 256>, 256, 0, a.count, 128, a, s);
+    case T_G4: return launch_persistent(k_group<4, 256>, 256, 0, a.count, 64, a, s);
+    case T_G8: return launch_persistent(k_group<8, 256>, 256, 0, a.count, 32, a, s);
+    case T_G16: return launch_persistent(k_group<16, 256>, 256, 0, a.count, 16, a, s);
+    case T_G32: return launch_persistent(k_group<32, 256>, 256, 0, a.count, 8, a, s);
+    case T_W64: return launch_persistent(k_warp_hash<6, 8>, 256, 8 * 64 * per_slot, a.count, 8, a, s);
+    case T_W128: return launch_persistent(k_warp_hash<7, 8>, 256, 8 * 128 * per_slot, a.count, 8, a, s);
+    case T_W256: return launch_persistent(k_warp_hash<8, 8>, 256, 8 * 256 * per_slot, a.count, 8, a, s);
+    case T_W512: return launch_persistent(k_warp_hash<9, 8>, 256, 8 * 512 * per_slot, a.count, 8, a, s);
+    case T_W1024: return launch_persistent(k_warp_hash<10, 4>, 128, 4 * 1024 * per_slot, a.count, 4, a, s);
+    case T_W2048: return launch_persistent(k_warp_hash<11, 4>, 128, 4 * 2048 * per_slot, a.count, 4, a, s);
+    case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
+    case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
+    case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sg

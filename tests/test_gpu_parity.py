@@ -1,0 +1,298 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle — SURVEY.md §8(c).
+
+Structure (row_ptr, col_idx) must be bit-exact; values exact in the integer / dyadic /
+coefficient modes and within 1e-12·Σ|a||b| in real mode.  Sizes span several tiles and
+ragged tails; every stage-2 class and the long-row growth path are exercised.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from util import compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "spec_examples.json")))
+
+
+@pytest.fixture(autouse=True)
+def _reset_debug():
+    import paper_1504_05022_b200 as sg
+    sg.set_debug(-1, 0, 0)
+    yield
+    sg.set_debug(-1, 0, 0)
+
+
+def _dense_csr(D, pattern=None):
+    D = np.asarray(D, dtype=np.float64)
+    mask = D != 0
+    for (r, c) in (pattern or []):
+        mask[r, c] = True
+    rows, cols = np.nonzero(mask)
+    return gen.from_coo(rows, cols, D.shape, vals=D[rows, cols])
+
+
+@pytest.mark.parametrize("case", GOLD["products"], ids=lambda c: c["cite"][:40])
+def test_golden(case):
+    A, B = _dense_csr(case["A"]), _dense_csr(case["B"])
+    g = run_gpu(A, B)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True)
+    assert g["u"].tolist() == case["u"]
+
+
+@pytest.mark.parametrize("mode", ["int", "real"])
+@pytest.mark.parametrize("shape,density", [((1, 1, 1), 1.0), ((37, 53, 41), 0.1), ((200, 150, 300), 0.05),
+                                           ((300, 300, 300), 0.2), ((64, 2000, 3000), 0.02)])
+def test_random(shape, density, mode):
+    m, k, n = shape
+    A = gen.random_csr(m, k, density, 11 + m, mode=mode, zero_frac=0.05)
+    B = gen.random_csr(k, n, density, 12 + n, mode=mode, zero_frac=0.05)
+    g = run_gpu(A, B)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=(mode == "int"))
+    u, _ = oracle.upper_bound(A, B)
+    np.testing.assert_array_equal(g["u"], u)
+
+
+BOUNDARY_U = [0, 1, 2, 3, 4, 5, 8, 9, 16, 17, 31, 32, 33, 51, 52, 64, 65, 102, 103, 204, 205, 409, 410, 819,
+              820, 1638, 1639, 2048, 2049, 4096, 4097, 8192, 8193, 9000]
+
+
+@pytest.mark.parametrize("dup", [0.0, 0.5, 0.95])
+def test_tier_boundaries(dup):
+    """Rows with u on both sides of every class threshold (SPEC acceptance 1 [S:482])."""
+    A, B = gen.forced_u_pair(BOUNDARY_U, n=20000, seed=5, mode="int", dup=dup)
+    g = run_gpu(A, B, stats=True)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True, what="dup=%s" % dup)
+    np.testing.assert_array_equal(g["u"], np.array(BOUNDARY_U))
+    assert np.all(np.diff(g["rp"]) <= g["u"])  # u_i >= nnz(c_i*) [S:211]
+
+
+def _classify(u, n):
+    """Python restatement of the stage-2 rule for the exact-integer check."""
+    if u == 0:
+        return 0
+    cap = min(u, n)
+    if u <= 32:
+        g = 0
+        while (1 << g) < u:
+            g += 1
+        return 1 + g
+    for t in range(7, 13):
+        if 4 * (64 << (t - 7)) >= 5 * cap:
+            return t
+    for t in range(13, 16):
+        if cap <= (2048 << (t - 13)):
+            return t
+    return 16
+
+
+def test_stage12_integers():
+    """Stage 1 U and the stage-2 class of every row, exactly."""
+    A, B = gen.forced_u_pair(BOUNDARY_U * 3, n=20000, seed=9, mode="int")
+    g = run_gpu(A, B, stats=True)
+    u, tot = oracle.upper_bound(A, B)
+    np.testing.assert_array_equal(g["u"], u)
+    assert g["stats"]["sum_u"] == tot
+    want = [_classify(int(x), B.shape[1]) for x in u]
+    np.testing.assert_array_equal(g["tier"], np.array(want))
+    counts = np.bincount(np.array(want), minlength=17)
+    from paper_1504_05022_b200 import TIER_NAMES
+    assert g["stats"]["tier_rows"] == {TIER_NAMES[t]: int(c) for t, c in enumerate(counts) if c}
+
+
+@pytest.mark.parametrize("tier", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16])
+def test_forced_tier(tier):
+    """Every row that a class can hold is routed through it; results agree with the oracle
+    (and so with every other class: P11 tier-forced agreement)."""
+    import paper_1504_05022_b200 as sg
+    us = [2, 3, 7, 16, 30, 32, 40, 100, 300, 700, 1500, 3000, 6000]
+    A, B = gen.forced_u_pair(us, n=9000, seed=tier, mode="int", dup=0.5)
+    sg.set_debug(tier, 0, 0)
+    g = run_gpu(A, B)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True, what="tier %d" % tier)
+
+
+@pytest.mark.parametrize("u", [600, 1500, 5000])
+@pytest.mark.parametrize("dup", [0.0, 0.5, 0.95])
+def test_long_growth(u, dup):
+    """Progressive re-allocation [P:297]: tiny initial capacity forces 1-6 growth rounds;
+    the resumed result equals the unbounded one [S:297] (SPEC acceptance 5 [S:487])."""
+    import paper_1504_05022_b200 as sg
+    us = [u, u // 2, 700, u]
+    A, B = gen.forced_u_pair(us, n=60000, seed=u + int(dup * 10), mode="int", dup=dup)
+    sg.set_debug(-1, 64, 40)  # long path for cap > 40, initial capacity 64
+    g = run_gpu(A, B, stats=True)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True, what="u=%d dup=%s" % (u, dup))
+    assert g["stats"]["long_rows"] == 4
+    assert g["stats"]["growth_rounds"] >= 1
+
+
+@pytest.mark.parametrize("flags_name", ["PRECISE", "UPPER_BOUND"])
+def test_strategies_equal(flags_name):
+    """Strategy invariance [S:213]: hybrid == precise == upper bound."""
+    import paper_1504_05022_b200 as sg
+    A = gen.rmat(11, 16, (0.57, 0.19, 0.19, 0.05), seed=3, mode="int")
+    R = oracle.spgemm(A, A)
+    sg.set_debug(-1, 256, 1000)
+    g = run_gpu(A, A, flags=getattr(sg, "FLAG_" + flags_name))
+    compare(g, R, exact=True, what=flags_name)
+    g2 = run_gpu(A, A, flags=0)
+    compare(g2, R, exact=True, what="hybrid")
+
+
+@pytest.mark.parametrize("kind,n", [("2d5", 32), ("2d9", 20), ("3d7", 12), ("3d27", 14)])
+def test_stencils(kind, n):
+    A = gen.stencil(kind, n)
+    g = run_gpu(A, A)
+    R = oracle.spgemm(A, A)
+    compare(g, R, exact=True, what=kind)
+
+
+def test_config1_full():
+    """BASELINE configs[0]: 2D 5-point 32×32, A² — full size, exact."""
+    A = gen.stencil("2d5", 32)
+    g = run_gpu(A, A, stats=True)
+    R = oracle.spgemm(A, A)
+    compare(g, R, exact=True)
+    assert g["nnz"] == 12676 and g["stats"]["sum_u"] == 24456
+
+
+@pytest.mark.parametrize("scale,abcd", [(12, (0.45, 0.15, 0.15, 0.25)), (13, (0.57, 0.19, 0.19, 0.05))])
+@pytest.mark.parametrize("mode", ["int", "real"])
+def test_rmat(scale, abcd, mode):
+    A = gen.rmat(scale, 16, abcd, seed=gen.SEED, mode=mode)
+    g = run_gpu(A, A)
+    R = oracle.spgemm(A, A)
+    compare(g, R, exact=(mode == "int"), what="rmat s%d" % scale)
+
+
+def test_rmat_long_rows_default_path():
+    """Graph500 skew at scale 14 has rows beyond every shared-memory class (T_LONG)."""
+    import paper_1504_05022_b200 as sg
+    A = gen.rmat(14, 16, (0.57, 0.19, 0.19, 0.05), seed=gen.SEED, mode="int")
+    sg.set_debug(-1, 2048, 0)
+    g = run_gpu(A, A, stats=True)
+    R = oracle.spgemm(A, A)
+    compare(g, R, exact=True)
+    assert g["stats"]["long_rows"] > 0
+
+
+@pytest.mark.parametrize("smoothed", [False, True])
+def test_galerkin(smoothed):
+    """Config 4 at 16³: both association orders; exact (dyadic values)."""
+    n = 16
+    A = gen.stencil("3d7", n)
+    P = gen.aggregation_P(n, smoothed=smoothed)
+    Rm = gen.transpose(P)
+    gAP = run_gpu(A, P)
+    oAP = oracle.spgemm(A, P)
+    compare(gAP, oAP, exact=True, what="AP")
+    AP = gen.Csr((A.shape[0], P.shape[1]), gAP["rp"], gAP["ci"], gAP["val"])
+    gRAP = run_gpu(Rm, AP)
+    oRAP = oracle.spgemm(Rm, AP)
+    compare(gRAP, oRAP, exact=True, what="R(AP)")
+    gRA = run_gpu(Rm, A)
+    RA = gen.Csr((Rm.shape[0], A.shape[1]), gRA["rp"], gRA["ci"], gRA["val"])
+    gRAP2 = run_gpu(RA, P)
+    np.testing.assert_array_equal(gRAP["rp"], gRAP2["rp"])
+    np.testing.assert_array_equal(gRAP["ci"], gRAP2["ci"])
+    np.testing.assert_array_equal(gRAP["val"], gRAP2["val"])
+    if not smoothed:
+        L = gen.stencil("3d7", n // 2)
+        np.testing.assert_array_equal(gRAP["ci"], L.ci)
+        np.testing.assert_array_equal(gRAP["val"], 4.0 * L.val)
+
+
+def test_band_uniform():
+    """Config 5 shape at n = 2^14: band(64) × uniform(64)."""
+    n = 1 << 14
+    A = gen.band(n, mode="real")
+    B = gen.uniform_rows(n, n, 64, mode="real")
+    g = run_gpu(A, B)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=False)
+
+
+def test_edge_cases():
+    # all rows empty
+    A = gen.Csr((5, 7), np.zeros(6, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    B = gen.random_csr(7, 9, 0.5, 1)
+    g = run_gpu(A, B)
+    assert g["nnz"] == 0 and g["rp"].tolist() == [0] * 6
+    # B empty (n columns but no entries)
+    A = gen.random_csr(6, 4, 0.5, 2)
+    B = gen.Csr((4, 3), np.zeros(5, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    g = run_gpu(A, B)
+    assert g["nnz"] == 0
+    # k = 0
+    A = gen.Csr((3, 0), np.zeros(4, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    B = gen.Csr((0, 5), np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    g = run_gpu(A, B)
+    assert g["nnz"] == 0 and g["rp"].tolist() == [0] * 4
+
+
+def test_m_zero():
+    import torch
+
+    import paper_1504_05022_b200 as sg
+    A = gen.Csr((0, 4), np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    B = gen.random_csr(4, 4, 0.5, 3)
+    op = sg.SpGEMM(sg.DeviceCsr.from_host(A), sg.DeviceCsr.from_host(B))
+    assert op.symbolic() == 0
+    C = op.numeric()
+    torch.cuda.synchronize()
+    assert C.rp.cpu().tolist() == [0]
+
+
+def test_determinism_and_cancellation():
+    A = gen.random_csr(400, 400, 0.05, 21, mode="real")
+    g1 = run_gpu(A, A)
+    g2 = run_gpu(A, A)
+    np.testing.assert_array_equal(g1["ci"], g2["ci"])
+    np.testing.assert_array_equal(g1["val"].view(np.int64), g2["val"].view(np.int64))
+    # explicit cancellation keeps a stored zero
+    A = _dense_csr([[1.0, 1.0]])
+    B = _dense_csr([[2.0], [-2.0]])
+    g = run_gpu(A, B)
+    assert g["nnz"] == 1 and g["val"][0] == 0.0
+
+
+def test_bitexact_warp_tiers_vs_oracle_real():
+    """Classes that accumulate in j-ascending order (G-lane sort, warp hash) reproduce
+    the oracle's rounding bit for bit in real mode (reading R1)."""
+    us = [2, 5, 9, 17, 32, 40, 100, 300, 700, 1500]
+    A, B = gen.forced_u_pair(us * 20, n=5000, seed=77, mode="real", dup=0.7)
+    g = run_gpu(A, B)
+    R = oracle.spgemm(A, B)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+
+
+def test_validate_flag():
+    import paper_1504_05022_b200 as sg
+    A = gen.random_csr(10, 10, 0.3, 4)
+    bad = gen.Csr(A.shape, A.rp, A.ci[::-1].copy(), A.val)
+    with pytest.raises(sg.SpgemmError) as e:
+        sg.SpGEMM(sg.DeviceCsr.from_host(bad), sg.DeviceCsr.from_host(A), sg.FLAG_VALIDATE)
+    assert e.value.status == 2
+    op = sg.SpGEMM(sg.DeviceCsr.from_host(A), sg.DeviceCsr.from_host(A), sg.FLAG_VALIDATE)
+    op.destroy()
+
+
+def test_numeric_before_symbolic():
+    import paper_1504_05022_b200 as sg
+    A = gen.random_csr(10, 10, 0.3, 4)
+    op = sg.SpGEMM(sg.DeviceCsr.from_host(A), sg.DeviceCsr.from_host(A))
+    with pytest.raises(sg.SpgemmError):
+        op.numeric()
+    op.destroy()
