@@ -286,6 +286,35 @@ spgemm_status_t run_long(spgemm_handle_t h, int mode) {
   return SPGEMM_SUCCESS;
 }
 
+// PRECISE numeric: exact tables (cap = nnz(c_i*)) for the rows of the numeric long class.
+spgemm_status_t prepare_long_exact(spgemm_handle_t h) {
+  const int64_t nl = h->nlong;
+  AL(h, &h->lst, nl);
+  AL(h, &h->lkeys, nl);
+  AL(h, &h->lvals, nl);
+  AL(h, &h->lold_keys, nl);
+  AL(h, &h->lold_vals, nl);
+  AL(h, &h->lold_slots, nl);
+  AL(h, &h->lovf, nl);
+  AL(h, &h->liota, nl);
+  AL(h, &h->lovf_cnt, 1);
+  AL(h, &h->lslots, nl);
+  AL(h, &h->lslot_off, nl + 1);
+  CK(h, cudaMemsetAsync(h->lkeys, 0, sizeof(int32_t*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lvals, 0, sizeof(double*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_vals, 0, sizeof(double*) * nl, h->stream));
+  CK(h, cudaMemsetAsync(h->lold_slots, 0, sizeof(int64_t) * nl, h->stream));
+  const unsigned g = (unsigned)((nl + 255) / 256);
+  k_iota<<<g, 256, 0, h->stream>>>(h->liota, nl);
+  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, 1, h->A, h->B, h->stream));
+  k_long_exact<<<g, 256, 0, h->stream>>>(h->lst, h->ws.perm, h->long_first, nl, h->nnz_row, h->A.rp,
+                                         h->lslots);
+  CK(h, cudaGetLastError());
+  h->long_entries = 0;
+  return long_alloc_tables(h, h->liota, nl, true, false);
+}
+
 }  // namespace
 
 extern "C" {
@@ -485,17 +514,6 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->tev_used[T_LONG] = true;
     h->launches_sym += 4 + 6 * h->growth_rounds;
   }
-  if (precise && h->nlong > 0) {
-    // exact tables for numeric (no growth: cap = nnz(c_i*)); allocated now so numeric never syncs
-    const unsigned g = (unsigned)((h->nlong + 255) / 256);
-    k_long_exact<<<g, 256, 0, h->stream>>>(h->lst, ws.perm, h->long_first, h->nlong, h->nnz_row,
-                                           h->A.rp, h->lslots);
-    CK(h, cudaGetLastError());
-    h->long_entries = 0;
-    s = long_alloc_tables(h, h->liota, h->nlong, true, false);
-    if (s != SPGEMM_SUCCESS) return s;
-    CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * h->nlong, h->stream));
-  }
   cudaEventRecord(h->ev[2], h->stream);
   // stage 4 (first half): sum the numbers of nonzero entries of all rows [P:301]
   CK(h, launch_exclusive_scan(h->nnz_row, h->c_rp, m, h->scan_tmp, h->stream));
@@ -506,6 +524,26 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   s = sync(h);
   if (s != SPGEMM_SUCCESS) return s;
   h->nnz_c = h->pinned[0];
+  if (precise) {
+    // numeric classes from the exact row lengths (tables sized by nnz(c_i*), not the bound)
+    CK(h, launch_rebin(m, h->n, h->nnz_row, tp, ws, h->stream));
+    h->launches_sym += 3;
+    CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
+    s = sync(h);
+    if (s != SPGEMM_SUCCESS) return s;
+    for (int t = 0; t < NUM_TIERS; ++t) {
+      h->tier_count[t] = h->pinned[kSumCount + t];
+      h->tier_off[t] = h->pinned[kSumOff + t];
+    }
+    h->tier_off[NUM_TIERS] = h->pinned[kSumOff + NUM_TIERS];
+    h->nlong = h->tier_count[T_LONG];
+    h->long_first = h->tier_off[T_LONG];
+    if (h->nlong > 0) {
+      s = prepare_long_exact(h);
+      if (s != SPGEMM_SUCCESS) return s;
+      h->launches_sym += 7;
+    }
+  }
   h->sym_ok = true;
   *c_nnz = h->nnz_c;
   return SPGEMM_SUCCESS;

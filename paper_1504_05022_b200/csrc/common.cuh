@@ -65,6 +65,32 @@ __host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
   return T_LONG;
 }
 
+// PRECISE numeric classes: the symbolic pass knows nnz(c_i*) exactly, so tables are sized
+// by it (load <= 1/2) instead of by the bound min(u_i, n).
+__host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
+  if (t == T_EMPTY) return u == 0;
+  if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
+  if (t >= T_W64 && t <= T_W2048) return 4 * (int64_t(64) << (t - T_W64)) >= 5 * nnz;
+  if (t >= T_C2048 && t <= T_C8192) return nnz <= (int64_t(2048) << (t - T_C2048));
+  return 1;
+}
+
+__host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, TierParams p) {
+  if (u == 0) return T_EMPTY;
+  if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz)) return p.force_tier;
+  if (p.long_threshold > 0 && nnz > p.long_threshold) return T_LONG;
+  if (u <= 32) {
+    int g = 0;
+    while ((int64_t(1) << g) < u) ++g;
+    return T_G1 + g;
+  }
+  for (int t = T_W64; t <= T_W2048; ++t)
+    if ((int64_t(64) << (t - T_W64)) >= 2 * nnz) return t;
+  for (int t = T_C2048; t <= T_C8192; ++t)
+    if (nnz <= (int64_t(2048) << (t - T_C2048))) return t;
+  return T_LONG;
+}
+
 // Hybrid C~ capacity of a row ([P:224]: u_i for short rows; here min(u_i, n) which is
 // still a safe bound since nnz(c_i*) <= n).  Long rows live in their own growing arena.
 __host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n) {
@@ -120,6 +146,9 @@ constexpr int kSumLen = kSumU + 3;
 cudaError_t launch_stage1(int64_t m, int64_t n, CsrView A, const int64_t* b_rp, TierParams tp,
                           bool hybrid_caps, Stage12Ws& ws, cudaStream_t s);
 cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n, cudaStream_t s);
+// PRECISE: re-bin rows by (u_i, nnz(c_i*)) into ws.tier/perm (ws.U and nnz_row are inputs).
+cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParams tp, Stage12Ws& ws,
+                         cudaStream_t s);
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
 

@@ -124,6 +124,35 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
   if (threadIdx.x < NUM_TIERS) blk_tier[int64_t(blockIdx.x) * NUM_TIERS + threadIdx.x] = s_hist[threadIdx.x];
 }
 
+// PRECISE: classes for the numeric pass from the exact row lengths of the symbolic pass.
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_t* __restrict__ U,
+                                              const int64_t* __restrict__ nnz_row, TierParams tp,
+                                              uint8_t* __restrict__ tier, int32_t* __restrict__ blk_tier,
+                                              int64_t* __restrict__ blk_cap, int64_t* __restrict__ blk_usum,
+                                              int64_t* __restrict__ blk_umax) {
+  __shared__ int s_hist[NUM_TIERS];
+  if (threadIdx.x < NUM_TIERS) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = int64_t(blockIdx.x) * NT * RPT;
+  for (int r = 0; r < RPT; ++r) {
+    const int64_t i = base + int64_t(r) * NT + threadIdx.x;
+    if (i < m) {
+      const int t = classify_exact(U[i], nnz_row[i], tp);
+      tier[i] = (uint8_t)t;
+      atomicAdd(&s_hist[t], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    blk_cap[blockIdx.x] = 0;
+    blk_usum[blockIdx.x] = 0;
+    blk_umax[blockIdx.x] = 0;
+  }
+  if (threadIdx.x < NUM_TIERS) blk_tier[int64_t(blockIdx.x) * NUM_TIERS + threadIdx.x] = s_hist[threadIdx.x];
+  (void)n;
+}
+
 // ---------------------------------------------------------------------------- stage 2
 // One CTA: per class, exclusive scan of per-block counts (class-major order, so perm holds
 // class 0 rows, then class 1 rows, ...); exclusive scan of per-block C~ capacities.
@@ -347,6 +376,16 @@ cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n,
   k_stage2_scatter<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
       m, n, hybrid_caps ? 1 : 0, ws.tier, ws.U, ws.blk_tier, ws.blk_cap, ws.perm, ws.ctil_off);
   return cudaGetLastError();
+}
+
+cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParams tp, Stage12Ws& ws,
+                         cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  k_rebin<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
+      m, n, ws.U, nnz_row, tp, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_stage2(m, ws, false, n, s);
 }
 
 int64_t scan_tmp_elems(int64_t len) { return (len + kScanTile - 1) / kScanTile + 2; }

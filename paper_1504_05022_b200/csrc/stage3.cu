@@ -163,56 +163,173 @@ __device__ __forceinline__ int ht_insert(int* keys, int c, unsigned mask, int sh
   }
 }
 
+// Register bitonic sort of N = 32·E int keys held in "blocked" layout (lane l holds
+// elements l·E .. l·E+E-1): strides < E are in-register, strides >= E cross lanes.
+template <int E>
+__device__ __forceinline__ void warp_bitonic_keys(int (&k)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int i = lane * E + r;
+          const int p = __shfl_xor_sync(0xffffffffu, k[r], lj);
+          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
+          k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (r & j) continue;
+          const int i = lane * E + r;
+          const bool asc = (i & kk) == 0;
+          const int x = k[r], y = k[r | j];
+          k[r] = asc ? min(x, y) : max(x, y);
+          k[r | j] = asc ? max(x, y) : min(x, y);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int ht_find(const int* keys, int c, unsigned mask, int shift) {
+  unsigned h = ((unsigned)c * 0x9E3779B1u) >> shift;
+  while (keys[h] != c) h = (h + 1) & mask;
+  return (int)h;
+}
+
+// Sorted output of a warp table: compact the keys into `scratch`, sort them (registers for
+// N <= 256, shared memory above), then fetch each key's value from the intact table.
+template <int E>
+__device__ __forceinline__ void warp_emit_sorted_reg(const int* keys, const double* vals, const int* scratch,
+                                                     int cnt, unsigned mask, int shift, int lane,
+                                                     int32_t* out_col, double* out_val) {
+  int k[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int i = lane * E + r;
+    k[r] = i < cnt ? scratch[i] : INT_MAX;
+  }
+  warp_bitonic_keys<E>(k, lane);
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int i = lane * E + r;
+    if (i < cnt) {
+      out_col[i] = k[r];
+      out_val[i] = vals[ht_find(keys, k[r], mask, shift)];
+    }
+  }
+}
+
 template <int LOG2S, int NW>
 __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
   constexpr int S = 1 << LOG2S;
+  constexpr unsigned MASK = S - 1;
+  constexpr int SHIFT = 32 - LOG2S;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool fill = a.mode == MODE_FILL;
-  int* keys = reinterpret_cast<int*>(smem) + w * S;
-  double* vals = reinterpret_cast<double*>(smem + size_t(NW) * S * sizeof(int)) + w * S;
+  // fill: [vals double S][keys int S][scratch int S] per warp; count: [keys int S]
+  double* vals = fill ? reinterpret_cast<double*>(smem) + size_t(w) * S : nullptr;
+  int* keys = fill ? reinterpret_cast<int*>(smem + size_t(NW) * S * sizeof(double)) + w * 2 * S
+                   : reinterpret_cast<int*>(smem) + w * S;
+  int* scratch = keys + S;
 
   for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
     const int row = __ldg(a.perm + a.first + r);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     for (int s = lane; s < S; s += 32) {
       keys[s] = kEmptyKey;
       if (fill) vals[s] = -0.0;  // -0.0 + x == x for every x: first add == "c_ik <- value"
     }
     __syncwarp();
-    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int inserted = 0;
     for (int64_t e0 = a0; e0 < a1; e0 += 32) {
       const int64_t e = e0 + lane;
-      int64_t bs = 0, be = 0;
+      int64_t bs = 0;
+      int len = 0;
       double av = 0.0;
       if (e < a1) {
         const int j = __ldg(a.A.ci + e);
         if (fill) av = __ldg(a.A.val + e);
         bs = __ldg(a.B.rp + j);
-        be = __ldg(a.B.rp + j + 1);
+        len = (int)(__ldg(a.B.rp + j + 1) - bs);
       }
       const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+      // software pipeline: the first 32 entries of b_j* for the next two a_ij are in flight
+      // while the current one is inserted (prefetch distance 2)
+      int c0 = kEmptyKey, c1 = kEmptyKey;
+      double v0 = 0.0, v1 = 0.0;
+      {
+        const int64_t b = __shfl_sync(0xffffffffu, bs, 0);
+        const int l = __shfl_sync(0xffffffffu, len, 0);
+        if (lane < l) {
+          c0 = __ldg(a.B.ci + b + lane);
+          if (fill) v0 = __ldg(a.B.val + b + lane);
+        }
+      }
+      if (nE > 1) {
+        const int64_t b = __shfl_sync(0xffffffffu, bs, 1);
+        const int l = __shfl_sync(0xffffffffu, len, 1);
+        if (lane < l) {
+          c1 = __ldg(a.B.ci + b + lane);
+          if (fill) v1 = __ldg(a.B.val + b + lane);
+        }
+      }
       for (int t = 0; t < nE; ++t) {
-        const int64_t jb = __shfl_sync(0xffffffffu, bs, t);
-        const int64_t je = __shfl_sync(0xffffffffu, be, t);
-        const double at = __shfl_sync(0xffffffffu, av, t);
-        for (int64_t q0 = jb; q0 < je; q0 += 32) {
-          const int64_t q = q0 + lane;
-          const bool act = q < je;
+        int c2 = kEmptyKey;
+        double v2 = 0.0;
+        if (t + 2 < nE) {
+          const int64_t b = __shfl_sync(0xffffffffu, bs, t + 2);
+          const int l = __shfl_sync(0xffffffffu, len, t + 2);
+          if (lane < l) {
+            c2 = __ldg(a.B.ci + b + lane);
+            if (fill) v2 = __ldg(a.B.val + b + lane);
+          }
+        }
+        const int lt = __shfl_sync(0xffffffffu, len, t);
+        const double at = fill ? __shfl_sync(0xffffffffu, av, t) : 0.0;
+        {
+          const bool act = lane < lt;
           int slot = 0;
-          double v = 0.0;
           if (act) {
-            const int c = __ldg(a.B.ci + q);
-            if (fill) v = __dmul_rn(at, __ldg(a.B.val + q));
             int isnew;
-            slot = ht_insert(keys, c, S - 1, 32 - LOG2S, isnew);
+            slot = ht_insert(keys, c0, MASK, SHIFT, isnew);
             inserted += isnew;
           }
           if (fill) {
             __syncwarp();
-            if (act) vals[slot] = __dadd_rn(vals[slot], v);
+            if (act) vals[slot] = __dadd_rn(vals[slot], __dmul_rn(at, v0));
           }
         }
+        if (lt > 32) {  // rest of a long b_j*, 32 columns per instruction
+          const int64_t bt = __shfl_sync(0xffffffffu, bs, t);
+          for (int q0 = 32; q0 < lt; q0 += 32) {
+            const int q = q0 + lane;
+            const bool act = q < lt;
+            int slot = 0;
+            double v = 0.0;
+            if (act) {
+              const int c = __ldg(a.B.ci + bt + q);
+              if (fill) v = __dmul_rn(at, __ldg(a.B.val + bt + q));
+              int isnew;
+              slot = ht_insert(keys, c, MASK, SHIFT, isnew);
+              inserted += isnew;
+            }
+            if (fill) {
+              __syncwarp();
+              if (act) vals[slot] = __dadd_rn(vals[slot], v);
+            }
+          }
+        }
+        c0 = c1;
+        v0 = v1;
+        c1 = c2;
+        v1 = v2;
       }
     }
     __syncwarp();
@@ -222,50 +339,53 @@ __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
       if (lane == 0 && a.nnz_row) a.nnz_row[row] = inserted;
       continue;
     }
-    // ordered compaction of occupied slots to the front
+    // compact the keys (slot order) into scratch; the table stays intact for value lookups
     int cnt = 0;
     for (int s0 = 0; s0 < S; s0 += 32) {
-      const int s = s0 + lane;
-      const int k = keys[s];
-      const double v = vals[s];
+      const int k = keys[s0 + lane];
       const bool occ = k != kEmptyKey;
       const unsigned bal = __ballot_sync(0xffffffffu, occ);
-      const int pos = cnt + __popc(bal & lanemask_lt());
-      __syncwarp();
-      if (occ) {
-        keys[pos] = k;
-        vals[pos] = v;
-      }
+      if (occ) scratch[cnt + __popc(bal & lanemask_lt())] = k;
       cnt += __popc(bal);
-      __syncwarp();
     }
-    int N = 1;
-    while (N < cnt) N <<= 1;
-    for (int s = cnt + lane; s < N; s += 32) keys[s] = INT_MAX;
     __syncwarp();
-    // bitonic sort of (key, value) in shared memory (the ESC sort, [P:277-284])
-    for (int k = 2; k <= N; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < (N >> 1); i += 32) {
-          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-          const int hi = lo + j;
-          const bool asc = (lo & k) == 0;
-          const int kl = keys[lo], kh = keys[hi];
-          if ((kl > kh) == asc) {
-            keys[lo] = kh;
-            keys[hi] = kl;
-            const double t = vals[lo];
-            vals[lo] = vals[hi];
-            vals[hi] = t;
-          }
-        }
-        __syncwarp();
-      }
-    }
     const int64_t o = __ldg(a.out_off + row);
-    for (int t = lane; t < cnt; t += 32) {
-      a.out_col[o + t] = keys[t];
-      a.out_val[o + t] = vals[t];
+    int32_t* oc = a.out_col + o;
+    double* ov = a.out_val + o;
+    if (cnt <= 32) {
+      warp_emit_sorted_reg<1>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
+    } else if (cnt <= 64) {
+      warp_emit_sorted_reg<2>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
+    } else if (cnt <= 128) {
+      warp_emit_sorted_reg<4>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
+    } else if (cnt <= 256) {
+      warp_emit_sorted_reg<8>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
+    } else {
+      // larger rows: bitonic sort of the scratch keys in shared memory (ESC sort [P:277-284])
+      int N = 1;
+      while (N < cnt) N <<= 1;
+      for (int s = cnt + lane; s < N; s += 32) scratch[s] = INT_MAX;
+      __syncwarp();
+      for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = lane; i < (N >> 1); i += 32) {
+            const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+            const int hi = lo + j;
+            const bool asc = (lo & k) == 0;
+            const int kl = scratch[lo], kh = scratch[hi];
+            if ((kl > kh) == asc) {
+              scratch[lo] = kh;
+              scratch[hi] = kl;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int t = lane; t < cnt; t += 32) {
+        const int k = scratch[t];
+        oc[t] = k;
+        ov[t] = vals[ht_find(keys, k, MASK, SHIFT)];
+      }
     }
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
     __syncwarp();
@@ -464,6 +584,7 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const bool fill = a.mode == MODE_FILL;
   const size_t per_slot = fill ? 12 : 4;
+  const size_t w_slot = fill ? 16 : 4;  // warp classes keep a key scratch for the sort
   switch (tier) {
     case T_G1: return launch_persistent(k_group<1, 256>, 256, 0, a.count, 256, a, s);
     case T_G2: return launch_persistent(k_group<2, 256>, 256, 0, a.count, 128, a, s);
@@ -471,12 +592,12 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_G8: return launch_persistent(k_group<8, 256>, 256, 0, a.count, 32, a, s);
     case T_G16: return launch_persistent(k_group<16, 256>, 256, 0, a.count, 16, a, s);
     case T_G32: return launch_persistent(k_group<32, 256>, 256, 0, a.count, 8, a, s);
-    case T_W64: return launch_persistent(k_warp_hash<6, 8>, 256, 8 * 64 * per_slot, a.count, 8, a, s);
-    case T_W128: return launch_persistent(k_warp_hash<7, 8>, 256, 8 * 128 * per_slot, a.count, 8, a, s);
-    case T_W256: return launch_persistent(k_warp_hash<8, 8>, 256, 8 * 256 * per_slot, a.count, 8, a, s);
-    case T_W512: return launch_persistent(k_warp_hash<9, 8>, 256, 8 * 512 * per_slot, a.count, 8, a, s);
-    case T_W1024: return launch_persistent(k_warp_hash<10, 4>, 128, 4 * 1024 * per_slot, a.count, 4, a, s);
-    case T_W2048: return launch_persistent(k_warp_hash<11, 4>, 128, 4 * 2048 * per_slot, a.count, 4, a, s);
+    case T_W64: return launch_persistent(k_warp_hash<6, 8>, 256, 8 * 64 * w_slot, a.count, 8, a, s);
+    case T_W128: return launch_persistent(k_warp_hash<7, 8>, 256, 8 * 128 * w_slot, a.count, 8, a, s);
+    case T_W256: return launch_persistent(k_warp_hash<8, 8>, 256, 8 * 256 * w_slot, a.count, 8, a, s);
+    case T_W512: return launch_persistent(k_warp_hash<9, 8>, 256, 8 * 512 * w_slot, a.count, 8, a, s);
+    case T_W1024: return launch_persistent(k_warp_hash<10, 4>, 128, 4 * 1024 * w_slot, a.count, 4, a, s);
+    case T_W2048: return launch_persistent(k_warp_hash<11, 4>, 128, 4 * 2048 * w_slot, a.count, 4, a, s);
     case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
     case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
     case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);
