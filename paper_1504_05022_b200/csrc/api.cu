@@ -464,8 +464,10 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   TierParams tp{g_force_tier, g_long_threshold};
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = false;
-  CK(h, launch_stage1(m, h->n, h->A, h->B.rp, tp, hybrid, ws, h->stream));
-  CK(h, launch_stage2(m, ws, hybrid, h->n, h->stream));
+  // C~ offsets in both strategies: hybrid keeps whole rows there, precise only the sorted
+  // column sets of the warp classes (4 B/entry) for its numeric pass
+  CK(h, launch_stage1(m, h->n, h->A, h->B.rp, tp, true, ws, h->stream));
+  CK(h, launch_stage2(m, ws, true, h->n, h->stream));
   h->launches_sym = 3;
   CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
   spgemm_status_t s = sync(h);
@@ -478,10 +480,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->sum_u = h->pinned[kSumU];
   h->sum_cap = h->pinned[kSumCap];
   h->max_u = h->pinned[kSumUMax];
-  if (hybrid) {
-    AL(h, &h->ctil_col, h->sum_cap);
-    AL(h, &h->ctil_val, h->sum_cap);
-  }
+  AL(h, &h->ctil_col, h->sum_cap);
+  if (hybrid) AL(h, &h->ctil_val, h->sum_cap);
   cudaEventRecord(h->ev[1], h->stream);
   // stage 3: one launch per non-empty class ([P:264] "only issue kernels for non-empty bins")
   for (int t = T_G1; t <= T_C8192; ++t) {
@@ -497,7 +497,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.out_col = h->ctil_col;
     a.out_val = h->ctil_val;
     a.nnz_row = h->nnz_row;
-    a.mode = hybrid ? MODE_FILL : MODE_COUNT;
+    a.mode = hybrid ? MODE_FILL : (t >= T_W64 && t <= T_W2048) ? MODE_STRUCT : MODE_COUNT;
     cudaEventRecord(h->tev[t][0], h->stream);
     CK(h, launch_stage3_tier(t, a, h->stream));
     cudaEventRecord(h->tev[t][1], h->stream);
@@ -590,7 +590,10 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.out_col = c_col_idx;
         a.out_val = c_val;
         a.nnz_row = nullptr;
-        a.mode = MODE_FILL;
+        const bool dense = t >= T_W64 && t <= T_W2048;
+        a.mode = dense ? MODE_DENSE : MODE_FILL;
+        a.struct_col = h->ctil_col;
+        a.struct_off = h->ws.ctil_off;
         cudaEventRecord(h->tev[t][0], h->stream);
         CK(h, launch_stage3_tier(t, a, h->stream));
         cudaEventRecord(h->tev[t][1], h->stream);
@@ -623,7 +626,8 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
       ca.m = 0;  // only the long rows are copied
     }
     const double avg = double(h->nnz_c) / double(h->m);
-    const int group = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    const int group = env_int("SPGEMM_COPY_GROUP", 0);  // 0 = flat warp copy (default)
+    (void)avg;
     CK(h, launch_copy(ca, group, h->stream));
     h->launches_num += (ca.m > 0 ? 1 : 0) + (ca.nlong > 0 ? 1 : 0);
   }

@@ -75,17 +75,24 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
   return 1;
 }
 
-__host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, TierParams p) {
+// sym_class: the row's symbolic class; warp classes in numeric need the sorted column set
+// that only the symbolic warp classes (STRUCT) produce.
+__host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_class, TierParams p) {
   if (u == 0) return T_EMPTY;
-  if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz)) return p.force_tier;
+  const bool has_struct = sym_class >= T_W64 && sym_class <= T_W2048;
+  if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz) &&
+      (has_struct || p.force_tier < T_W64 || p.force_tier > T_W2048) &&
+      !(p.force_tier >= T_G1 && p.force_tier <= T_G32 && has_struct))
+    return p.force_tier;
   if (p.long_threshold > 0 && nnz > p.long_threshold) return T_LONG;
-  if (u <= 32) {
+  if (u <= 32 && !has_struct) {
     int g = 0;
     while ((int64_t(1) << g) < u) ++g;
     return T_G1 + g;
   }
-  for (int t = T_W64; t <= T_W2048; ++t)
-    if ((int64_t(64) << (t - T_W64)) >= 2 * nnz) return t;
+  if (has_struct)
+    for (int t = T_W64; t <= T_W2048; ++t)
+      if ((int64_t(64) << (t - T_W64)) >= 2 * nnz) return t;
   for (int t = T_C2048; t <= T_C8192; ++t)
     if (nnz <= (int64_t(2048) << (t - T_C2048))) return t;
   return T_LONG;
@@ -104,7 +111,11 @@ struct CsrView {
   const double* val;
 };
 
-enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1 };
+// COUNT: nnz(c_i*) only.  FILL: sorted row with values (C~ in hybrid, C in precise numeric).
+// STRUCT (precise symbolic): nnz(c_i*) and the sorted column set of the row, written to
+// out_col at out_off.  DENSE (precise numeric): values from the sorted column set of STRUCT,
+// accumulated into a dense, already ordered array (no insertion, no sort).
+enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1, MODE_STRUCT = 2, MODE_DENSE = 3 };
 
 struct Stage3Args {
   CsrView A, B;
@@ -117,6 +128,8 @@ struct Stage3Args {
   double* out_val;
   int64_t* nnz_row;        // per-row nnz (written in both modes; may be NULL in numeric)
   int mode;
+  const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
+  const int64_t* struct_off;  // DENSE: their per-row offsets
 };
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
   for (int r = 0; r < RPT; ++r) {
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     if (i < m) {
-      const int t = classify_exact(U[i], nnz_row[i], tp);
+      const int t = classify_exact(U[i], nnz_row[i], (int)tier[i], tp);
       tier[i] = (uint8_t)t;
       atomicAdd(&s_hist[t], 1);
     }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int
       int pos = s_run[t] + wrank;
       for (int k = 0; k < w; ++k) pos += s_wcnt[k][t];
       perm[pos] = (int32_t)i;
-      ctil_off[i] = cap_carry + ex;
+      if (hybrid) ctil_off[i] = cap_carry + ex;
     }
     cap_carry += tot;
     __syncthreads();

@@ -138,31 +138,7 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
   }
 }
 
-// --------------------------------------------------------------- warp hash (T_W*)
-__device__ __forceinline__ int ht_insert(int* keys, int c, unsigned mask, int shift, int& isnew) {
-  unsigned h = ((unsigned)c * 0x9E3779B1u) >> shift;
-  volatile int* vk = keys;
-  while (true) {
-    const int k = vk[h];
-    if (k == c) {
-      isnew = 0;
-      return (int)h;
-    }
-    if (k == kEmptyKey) {
-      const int old = atomicCAS(&keys[h], kEmptyKey, c);
-      if (old == kEmptyKey) {
-        isnew = 1;
-        return (int)h;
-      }
-      if (old == c) {
-        isnew = 0;
-        return (int)h;
-      }
-    }
-    h = (h + 1) & mask;
-  }
-}
-
+// --------------------------------------------------------------- warp classes
 // Register bitonic sort of N = 32·E int keys held in "blocked" layout (lane l holds
 // elements l·E .. l·E+E-1): strides < E are in-register, strides >= E cross lanes.
 template <int E>
@@ -203,8 +179,8 @@ __device__ __forceinline__ int ht_find(const int* keys, int c, unsigned mask, in
 }
 
 // Sorted output of a warp table: compact the keys into `scratch`, sort them (registers for
-// N <= 256, shared memory above), then fetch each key's value from the intact table.
-template <int E>
+// N <= 128, shared memory above), then fetch each key's value from the intact table.
+template <int E, bool VALS>
 __device__ __forceinline__ void warp_emit_sorted_reg(const int* keys, const double* vals, const int* scratch,
                                                      int cnt, unsigned mask, int shift, int lane,
                                                      int32_t* out_col, double* out_val) {
@@ -220,110 +196,250 @@ __device__ __forceinline__ void warp_emit_sorted_reg(const int* keys, const doub
     const int i = lane * E + r;
     if (i < cnt) {
       out_col[i] = k[r];
-      out_val[i] = vals[ht_find(keys, k[r], mask, shift)];
+      if (VALS) out_val[i] = vals[ht_find(keys, k[r], mask, shift)];
     }
   }
 }
 
-template <int LOG2S, int NW>
+template <bool VALS>
+__device__ __forceinline__ void warp_emit_sorted(const int* keys, const double* vals, int* scratch, int cnt,
+                                                 unsigned mask, int shift, int lane, int32_t* oc, double* ov) {
+  if (cnt <= 32) {
+    warp_emit_sorted_reg<1, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
+  } else if (cnt <= 64) {
+    warp_emit_sorted_reg<2, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
+  } else if (cnt <= 128) {
+    warp_emit_sorted_reg<4, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
+  } else {
+    // larger rows: bitonic sort of the scratch keys in shared memory (ESC sort [P:277-284])
+    int N = 1;
+    while (N < cnt) N <<= 1;
+    for (int s = cnt + lane; s < N; s += 32) scratch[s] = INT_MAX;
+    __syncwarp();
+    for (int kk = 2; kk <= N; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < (N >> 1); i += 32) {
+          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          const int hi = lo + j;
+          const bool asc = (lo & kk) == 0;
+          const int kl = scratch[lo], kh = scratch[hi];
+          if ((kl > kh) == asc) {
+            scratch[lo] = kh;
+            scratch[hi] = kl;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int t = lane; t < cnt; t += 32) {
+      const int kk = scratch[t];
+      oc[t] = kk;
+      if (VALS) ov[t] = vals[ht_find(keys, kk, mask, shift)];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Warp classes.  One warp per row; lanes walk one b_j* at a time (columns within a row of B
+// are distinct, so no two lanes of one instruction touch one slot).  The next two b_j* are
+// in flight while one is processed (prefetch distance 2).  Tables are static shared arrays
+// so every access is a direct 32-bit shared address.
+//   MODE_COUNT  : insert keys, count                       (precise symbolic, non-warp rows)
+//   MODE_STRUCT : insert keys, count, emit the sorted set  (precise symbolic)
+//   MODE_FILL   : insert keys + accumulate values, emit the sorted row   (hybrid)
+template <int NW>
+struct WarpMeta {
+  const int32_t* pc[NW][32];
+  const double* pv[NW][32];
+  int len[NW][32];
+  double av[NW][32];
+};
+
+// stage up to 32 a_ij of the row: pointers to b_j* and lengths
+template <int NW, bool VALS>
+__device__ __forceinline__ int stage_a_chunk(const Stage3Args& a, WarpMeta<NW>& m, int w, int lane,
+                                             int64_t e0, int64_t a1) {
+  const int64_t e = e0 + lane;
+  const int32_t* pc = a.B.ci;
+  const double* pv = a.B.val;
+  int len = 0;
+  double av = 0.0;
+  if (e < a1) {
+    const int j = __ldg(a.A.ci + e);
+    if (VALS) av = __ldg(a.A.val + e);
+    const int64_t bs = __ldg(a.B.rp + j);
+    len = (int)(__ldg(a.B.rp + j + 1) - bs);
+    pc += bs;
+    pv += bs;
+  }
+  m.pc[w][lane] = pc;
+  m.pv[w][lane] = pv;
+  m.len[w][lane] = len;
+  m.av[w][lane] = av;
+  __syncwarp();
+  return (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+}
+
+template <int LOG2S>
+__device__ __forceinline__ unsigned hslot(int c) {
+  return ((unsigned)c * 0x9E3779B1u) >> (32 - LOG2S);
+}
+
+// insert c (if act) into keys[]: warp-uniform probing rounds; returns the slot
+template <int LOG2S>
+__device__ __forceinline__ unsigned warp_insert(int* keys, int c, bool act, int& inserted) {
+  constexpr unsigned MASK = (1u << LOG2S) - 1;
+  unsigned h = hslot<LOG2S>(c);
+  int k = keys[h];
+  bool pend = act && k != c;
+  while (__any_sync(0xffffffffu, pend)) {
+    if (pend) {
+      if (k == kEmptyKey) {
+        const int old = atomicCAS(&keys[h], kEmptyKey, c);
+        if (old == kEmptyKey || old == c) {
+          inserted += old == kEmptyKey;
+          pend = false;
+        } else {
+          h = (h + 1) & MASK;
+          k = keys[h];
+        }
+      } else if (k == c) {
+        pend = false;
+      } else {
+        h = (h + 1) & MASK;
+        k = *(volatile int*)&keys[h];
+      }
+    }
+  }
+  return h;
+}
+
+// Runtime-size variant (symbolic tables that grow): lg = log2 of the current size.
+__device__ __forceinline__ unsigned warp_insert_rt(int* keys, int c, bool act, int lg, int& inserted) {
+  const unsigned mask = (1u << lg) - 1;
+  unsigned h = ((unsigned)c * 0x9E3779B1u) >> (32 - lg);
+  int k = keys[h];
+  bool pend = act && k != c;
+  while (__any_sync(0xffffffffu, pend)) {
+    if (pend) {
+      if (k == kEmptyKey) {
+        const int old = atomicCAS(&keys[h], kEmptyKey, c);
+        if (old == kEmptyKey || old == c) {
+          inserted += old == kEmptyKey;
+          pend = false;
+        } else {
+          h = (h + 1) & mask;
+          k = keys[h];
+        }
+      } else if (k == c) {
+        pend = false;
+      } else {
+        h = (h + 1) & mask;
+        k = *(volatile int*)&keys[h];
+      }
+    }
+  }
+  return h;
+}
+
+// Double the table (keys only): move the keys to scratch, clear, reinsert.
+__device__ __forceinline__ void warp_grow(int* keys, int* scratch, int& lg, int lane) {
+  const int S = 1 << lg;
+  int n = 0;
+  for (int s0 = 0; s0 < S; s0 += 32) {
+    const int kk = keys[s0 + lane];
+    const bool occ = kk != kEmptyKey;
+    const unsigned bal = __ballot_sync(0xffffffffu, occ);
+    if (occ) scratch[n + __popc(bal & lanemask_lt())] = kk;
+    n += __popc(bal);
+  }
+  __syncwarp();
+  ++lg;
+  for (int s = lane; s < 2 * S; s += 32) keys[s] = kEmptyKey;
+  __syncwarp();
+  int dummy = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const bool act = i0 + lane < n;
+    warp_insert_rt(keys, act ? scratch[i0 + lane] : kEmptyKey, act, lg, dummy);
+  }
+  __syncwarp();
+}
+
+template <int LOG2S, int NW, int MODE>
 __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
+  constexpr bool FILL = MODE == MODE_FILL;
+  constexpr bool SORTED = MODE != MODE_COUNT;
   constexpr int S = 1 << LOG2S;
-  constexpr unsigned MASK = S - 1;
-  constexpr int SHIFT = 32 - LOG2S;
-  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_keys[NW][S];
+  __shared__ int s_scratch[SORTED ? NW : 1][SORTED ? S : 1];
+  __shared__ double s_vals[FILL ? NW : 1][FILL ? S : 1];
+  __shared__ WarpMeta<NW> meta;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const bool fill = a.mode == MODE_FILL;
-  // fill: [vals double S][keys int S][scratch int S] per warp; count: [keys int S]
-  double* vals = fill ? reinterpret_cast<double*>(smem) + size_t(w) * S : nullptr;
-  int* keys = fill ? reinterpret_cast<int*>(smem + size_t(NW) * S * sizeof(double)) + w * 2 * S
-                   : reinterpret_cast<int*>(smem) + w * S;
-  int* scratch = keys + S;
+  int* keys = s_keys[w];
+  // symbolic modes start from a small table and double it when the load would pass 3/4
+  // (the count is not known yet: only the bound min(u_i, n) sized the class)
+  constexpr int LG0 = (MODE == MODE_STRUCT && LOG2S > 8) ? 8 : LOG2S;
+  int* gscratch = s_scratch[SORTED ? w : 0];
 
   for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    for (int s = lane; s < S; s += 32) {
+    int lg = LG0;
+#pragma unroll 4
+    for (int s = lane; s < (1 << LG0); s += 32) {
       keys[s] = kEmptyKey;
-      if (fill) vals[s] = -0.0;  // -0.0 + x == x for every x: first add == "c_ik <- value"
+      if (FILL) s_vals[w][s] = -0.0;  // -0.0 + x == x: the first add is "c_ik <- value"
     }
-    __syncwarp();
-    int inserted = 0;
+    int inserted = 0;  // per lane
+    int total = 0;     // warp-uniform (non-FILL modes)
     for (int64_t e0 = a0; e0 < a1; e0 += 32) {
-      const int64_t e = e0 + lane;
-      int64_t bs = 0;
-      int len = 0;
-      double av = 0.0;
-      if (e < a1) {
-        const int j = __ldg(a.A.ci + e);
-        if (fill) av = __ldg(a.A.val + e);
-        bs = __ldg(a.B.rp + j);
-        len = (int)(__ldg(a.B.rp + j + 1) - bs);
-      }
-      const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
-      // software pipeline: the first 32 entries of b_j* for the next two a_ij are in flight
-      // while the current one is inserted (prefetch distance 2)
+      const int nE = stage_a_chunk<NW, FILL>(a, meta, w, lane, e0, a1);
       int c0 = kEmptyKey, c1 = kEmptyKey;
       double v0 = 0.0, v1 = 0.0;
-      {
-        const int64_t b = __shfl_sync(0xffffffffu, bs, 0);
-        const int l = __shfl_sync(0xffffffffu, len, 0);
-        if (lane < l) {
-          c0 = __ldg(a.B.ci + b + lane);
-          if (fill) v0 = __ldg(a.B.val + b + lane);
-        }
+      if (lane < meta.len[w][0]) {
+        c0 = __ldg(meta.pc[w][0] + lane);
+        if (FILL) v0 = __ldg(meta.pv[w][0] + lane);
       }
-      if (nE > 1) {
-        const int64_t b = __shfl_sync(0xffffffffu, bs, 1);
-        const int l = __shfl_sync(0xffffffffu, len, 1);
-        if (lane < l) {
-          c1 = __ldg(a.B.ci + b + lane);
-          if (fill) v1 = __ldg(a.B.val + b + lane);
-        }
+      if (nE > 1 && lane < meta.len[w][1]) {
+        c1 = __ldg(meta.pc[w][1] + lane);
+        if (FILL) v1 = __ldg(meta.pv[w][1] + lane);
       }
       for (int t = 0; t < nE; ++t) {
         int c2 = kEmptyKey;
         double v2 = 0.0;
-        if (t + 2 < nE) {
-          const int64_t b = __shfl_sync(0xffffffffu, bs, t + 2);
-          const int l = __shfl_sync(0xffffffffu, len, t + 2);
-          if (lane < l) {
-            c2 = __ldg(a.B.ci + b + lane);
-            if (fill) v2 = __ldg(a.B.val + b + lane);
+        if (t + 2 < nE && lane < meta.len[w][t + 2]) {
+          c2 = __ldg(meta.pc[w][t + 2] + lane);
+          if (FILL) v2 = __ldg(meta.pv[w][t + 2] + lane);
+        }
+        const int lt = meta.len[w][t];
+        if (FILL) {
+          const unsigned h = warp_insert<LOG2S>(keys, c0, lane < lt, inserted);  // lines 7-8
+          __syncwarp();
+          if (lane < lt) s_vals[w][h] = __dadd_rn(s_vals[w][h], __dmul_rn(meta.av[w][t], v0));
+        } else {
+          for (int q0 = 0; q0 < lt; q0 += 32) {
+            const int add = min(32, lt - q0);
+            if (4 * (total + add) > 3 * (1 << lg) && lg < LOG2S) {
+              do {
+                warp_grow(keys, gscratch, lg, lane);
+              } while (4 * (total + add) > 3 * (1 << lg) && lg < LOG2S);
+            }
+            const bool act = q0 + lane < lt;
+            const int c = q0 == 0 ? c0 : (act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey);
+            int nw = 0;
+            warp_insert_rt(keys, c, act, lg, nw);
+            inserted += nw;
+            total += __popc(__ballot_sync(0xffffffffu, nw != 0));
           }
         }
-        const int lt = __shfl_sync(0xffffffffu, len, t);
-        const double at = fill ? __shfl_sync(0xffffffffu, av, t) : 0.0;
-        {
-          const bool act = lane < lt;
-          int slot = 0;
-          if (act) {
-            int isnew;
-            slot = ht_insert(keys, c0, MASK, SHIFT, isnew);
-            inserted += isnew;
-          }
-          if (fill) {
-            __syncwarp();
-            if (act) vals[slot] = __dadd_rn(vals[slot], __dmul_rn(at, v0));
-          }
-        }
-        if (lt > 32) {  // rest of a long b_j*, 32 columns per instruction
-          const int64_t bt = __shfl_sync(0xffffffffu, bs, t);
+        if (FILL && lt > 32) {  // rest of a long b_j*, 32 columns per instruction
           for (int q0 = 32; q0 < lt; q0 += 32) {
-            const int q = q0 + lane;
-            const bool act = q < lt;
-            int slot = 0;
-            double v = 0.0;
-            if (act) {
-              const int c = __ldg(a.B.ci + bt + q);
-              if (fill) v = __dmul_rn(at, __ldg(a.B.val + bt + q));
-              int isnew;
-              slot = ht_insert(keys, c, MASK, SHIFT, isnew);
-              inserted += isnew;
-            }
-            if (fill) {
-              __syncwarp();
-              if (act) vals[slot] = __dadd_rn(vals[slot], v);
-            }
+            const bool act = q0 + lane < lt;
+            const int c = act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey;
+            const unsigned hh = warp_insert<LOG2S>(keys, c, act, inserted);
+            const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
+            __syncwarp();
+            if (act) s_vals[w][hh] = __dadd_rn(s_vals[w][hh], __dmul_rn(meta.av[w][t], v));
           }
         }
         c0 = c1;
@@ -331,63 +447,131 @@ __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
         c1 = c2;
         v1 = v2;
       }
+      __syncwarp();
     }
-    __syncwarp();
-    if (!fill) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+    for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+    if (!SORTED) {
       if (lane == 0 && a.nnz_row) a.nnz_row[row] = inserted;
+      __syncwarp();
       continue;
     }
-    // compact the keys (slot order) into scratch; the table stays intact for value lookups
-    int cnt = 0;
-    for (int s0 = 0; s0 < S; s0 += 32) {
-      const int k = keys[s0 + lane];
-      const bool occ = k != kEmptyKey;
+    const int cnt = inserted;
+    int* scratch = gscratch;
+    int base = 0;
+#pragma unroll 4
+    for (int s0 = 0; s0 < (1 << lg); s0 += 32) {
+      const int kk = keys[s0 + lane];
+      const bool occ = kk != kEmptyKey;
       const unsigned bal = __ballot_sync(0xffffffffu, occ);
-      if (occ) scratch[cnt + __popc(bal & lanemask_lt())] = k;
-      cnt += __popc(bal);
+      if (occ) scratch[base + __popc(bal & lanemask_lt())] = kk;
+      base += __popc(bal);
     }
     __syncwarp();
     const int64_t o = __ldg(a.out_off + row);
-    int32_t* oc = a.out_col + o;
-    double* ov = a.out_val + o;
-    if (cnt <= 32) {
-      warp_emit_sorted_reg<1>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
-    } else if (cnt <= 64) {
-      warp_emit_sorted_reg<2>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
-    } else if (cnt <= 128) {
-      warp_emit_sorted_reg<4>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
-    } else if (cnt <= 256) {
-      warp_emit_sorted_reg<8>(keys, vals, scratch, cnt, MASK, SHIFT, lane, oc, ov);
-    } else {
-      // larger rows: bitonic sort of the scratch keys in shared memory (ESC sort [P:277-284])
-      int N = 1;
-      while (N < cnt) N <<= 1;
-      for (int s = cnt + lane; s < N; s += 32) scratch[s] = INT_MAX;
-      __syncwarp();
-      for (int k = 2; k <= N; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = lane; i < (N >> 1); i += 32) {
-            const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-            const int hi = lo + j;
-            const bool asc = (lo & k) == 0;
-            const int kl = scratch[lo], kh = scratch[hi];
-            if ((kl > kh) == asc) {
-              scratch[lo] = kh;
-              scratch[hi] = kl;
+    warp_emit_sorted<FILL>(keys, FILL ? s_vals[FILL ? w : 0] : nullptr, scratch, cnt, (1u << lg) - 1,
+                           32 - lg, lane, a.out_col + o, FILL ? a.out_val + o : nullptr);
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+    __syncwarp();
+  }
+}
+
+// PRECISE numeric, warp classes: the symbolic pass (STRUCT) left the row's sorted column set
+// at struct_col + struct_off[row].  Build a read-only key -> position table, accumulate each
+// product into vals[position] (positions are distinct within one b_j*; j-ascending order
+// across them: the oracle's order) and write C's row in order: no insertion, no sort.
+template <int LOG2S, int NW>
+__global__ void __launch_bounds__(NW * 32) k_warp_dense(Stage3Args a) {
+  constexpr int S = 1 << LOG2S;
+  constexpr unsigned MASK = S - 1;
+  __shared__ int2 s_tab[NW][S];
+  __shared__ double s_vals[NW][S / 2];
+  __shared__ WarpMeta<NW> meta;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int2* tab = s_tab[w];
+  double* vals = s_vals[w];
+
+  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t o = __ldg(a.out_off + row);
+    const int nnz = (int)(__ldg(a.out_off + row + 1) - o);
+    const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
+#pragma unroll 4
+    for (int s = lane; s < S; s += 32) tab[s].x = kEmptyKey;
+    for (int p = lane; p < nnz; p += 32) vals[p] = -0.0;  // identity of +: first add == line 9
+    __syncwarp();
+    for (int p = lane; p < nnz; p += 32) {
+      const int c = __ldg(sc + p);
+      a.out_col[o + p] = c;  // C's columns: the sorted set itself
+      unsigned h = hslot<LOG2S>(c);
+      while (atomicCAS(&tab[h].x, kEmptyKey, c) != kEmptyKey) h = (h + 1) & MASK;
+      tab[h].y = p;
+    }
+    __syncwarp();
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+      const int nE = stage_a_chunk<NW, true>(a, meta, w, lane, e0, a1);
+      int c0 = kEmptyKey, c1 = kEmptyKey;
+      double v0 = 0.0, v1 = 0.0;
+      if (lane < meta.len[w][0]) {
+        c0 = __ldg(meta.pc[w][0] + lane);
+        v0 = __ldg(meta.pv[w][0] + lane);
+      }
+      if (nE > 1 && lane < meta.len[w][1]) {
+        c1 = __ldg(meta.pc[w][1] + lane);
+        v1 = __ldg(meta.pv[w][1] + lane);
+      }
+      for (int t = 0; t < nE; ++t) {
+        int c2 = kEmptyKey;
+        double v2 = 0.0;
+        if (t + 2 < nE && lane < meta.len[w][t + 2]) {
+          c2 = __ldg(meta.pc[w][t + 2] + lane);
+          v2 = __ldg(meta.pv[w][t + 2] + lane);
+        }
+        const int lt = meta.len[w][t];
+        const double at = meta.av[w][t];
+        {
+          const bool act = lane < lt;
+          unsigned h = hslot<LOG2S>(c0);
+          int2 kv = tab[h];
+          bool pend = act && kv.x != c0;
+          while (__any_sync(0xffffffffu, pend)) {
+            if (pend) {
+              h = (h + 1) & MASK;
+              kv = tab[h];
+              pend = kv.x != c0;
             }
           }
           __syncwarp();
+          if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v0));  // line 11
         }
+        if (lt > 32) {
+          for (int q0 = 32; q0 < lt; q0 += 32) {
+            const bool act = q0 + lane < lt;
+            const int c = act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey;
+            const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
+            unsigned h = hslot<LOG2S>(c);
+            int2 kv = tab[h];
+            bool pend = act && kv.x != c;
+            while (__any_sync(0xffffffffu, pend)) {
+              if (pend) {
+                h = (h + 1) & MASK;
+                kv = tab[h];
+                pend = kv.x != c;
+              }
+            }
+            __syncwarp();
+            if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v));
+          }
+        }
+        c0 = c1;
+        v0 = v1;
+        c1 = c2;
+        v1 = v2;
       }
-      for (int t = lane; t < cnt; t += 32) {
-        const int k = scratch[t];
-        oc[t] = k;
-        ov[t] = vals[ht_find(keys, k, MASK, SHIFT)];
-      }
+      __syncwarp();
     }
-    if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+    for (int p = lane; p < nnz; p += 32) a.out_val[o + p] = vals[p];
     __syncwarp();
   }
 }
@@ -582,9 +766,8 @@ cudaError_t launch_persistent(K kernel, int nt, size_t dsmem, int64_t work_units
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  const bool fill = a.mode == MODE_FILL;
+  const bool fill = a.mode == MODE_FILL || a.mode == MODE_DENSE;
   const size_t per_slot = fill ? 12 : 4;
-  const size_t w_slot = fill ? 16 : 4;  // warp classes keep a key scratch for the sort
   switch (tier) {
     case T_G1: return launch_persistent(k_group<1, 256>, 256, 0, a.count, 256, a, s);
     case T_G2: return launch_persistent(k_group<2, 256>, 256, 0, a.count, 128, a, s);
@@ -592,12 +775,36 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_G8: return launch_persistent(k_group<8, 256>, 256, 0, a.count, 32, a, s);
     case T_G16: return launch_persistent(k_group<16, 256>, 256, 0, a.count, 16, a, s);
     case T_G32: return launch_persistent(k_group<32, 256>, 256, 0, a.count, 8, a, s);
-    case T_W64: return launch_persistent(k_warp_hash<6, 8>, 256, 8 * 64 * w_slot, a.count, 8, a, s);
-    case T_W128: return launch_persistent(k_warp_hash<7, 8>, 256, 8 * 128 * w_slot, a.count, 8, a, s);
-    case T_W256: return launch_persistent(k_warp_hash<8, 8>, 256, 8 * 256 * w_slot, a.count, 8, a, s);
-    case T_W512: return launch_persistent(k_warp_hash<9, 8>, 256, 8 * 512 * w_slot, a.count, 8, a, s);
-    case T_W1024: return launch_persistent(k_warp_hash<10, 4>, 128, 4 * 1024 * w_slot, a.count, 4, a, s);
-    case T_W2048: return launch_persistent(k_warp_hash<11, 4>, 128, 4 * 2048 * w_slot, a.count, 4, a, s);
+    case T_W64:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<6, 8>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<6, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<6, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
+      return launch_persistent(k_warp_hash<6, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
+    case T_W128:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<7, 8>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<7, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<7, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
+      return launch_persistent(k_warp_hash<7, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
+    case T_W256:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<8, 8>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<8, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<8, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
+      return launch_persistent(k_warp_hash<8, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
+    case T_W512:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<9, 4>, 128, 0, a.count, 4, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<9, 4, MODE_FILL>, 128, 0, a.count, 4, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<9, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
+      return launch_persistent(k_warp_hash<9, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
+    case T_W1024:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<10, 2>, 64, 0, a.count, 2, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<10, 2, MODE_FILL>, 64, 0, a.count, 2, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<10, 4, MODE_STRUCT>, 128, 0, a.count, 4, a, s);
+      return launch_persistent(k_warp_hash<10, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
+    case T_W2048:
+      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<11, 1>, 32, 0, a.count, 1, a, s);
+      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<11, 1, MODE_FILL>, 32, 0, a.count, 1, a, s);
+      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<11, 2, MODE_STRUCT>, 64, 0, a.count, 2, a, s);
+      return launch_persistent(k_warp_hash<11, 4, MODE_COUNT>, 128, 0, a.count, 4, a, s);
     case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
     case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
     case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);

@@ -31,6 +31,43 @@ __global__ void __launch_bounds__(256) k_copy(CopyArgs a) {
   }
 }
 
+// Flat copy: warp w owns rows [32w, 32w+32); their outputs form one contiguous span of C.
+// Lane p-th output finds its row by a shuffle binary search over the 33 row pointers, so
+// every store instruction writes 32 consecutive entries.
+__global__ void __launch_bounds__(256) k_copy_flat(CopyArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (a.m + 31) / 32;
+  for (int64_t wi = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; wi < nwarps;
+       wi += int64_t(gridDim.x) * blockDim.x / 32) {
+    const int64_t i0 = wi * 32;
+    const int64_t i = i0 + lane;
+    const bool has = i < a.m;
+    const int64_t rp = has ? __ldg(a.c_rp + i) : __ldg(a.c_rp + a.m);
+    const int64_t end = __shfl_sync(0xffffffffu, has ? __ldg(a.c_rp + i + 1) : rp, 31);
+    const int64_t beg = __shfl_sync(0xffffffffu, rp, 0);
+    const int64_t src = has ? __ldg(a.ctil_off + i) : 0;
+    const bool lng = has && a.tier[i] == T_LONG;
+    for (int64_t p0 = beg; p0 < end; p0 += 32) {
+      const int64_t p = p0 + lane;
+      // last lane k with rp_k <= p (rows are ascending; empty rows share rp values)
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int64_t v = __shfl_sync(0xffffffffu, rp, lo + step);
+        if (lo + step < 32 && v <= p) lo += step;
+      }
+      const int64_t rbeg = __shfl_sync(0xffffffffu, rp, lo);
+      const int64_t rsrc = __shfl_sync(0xffffffffu, src, lo);
+      const bool rl = __shfl_sync(0xffffffffu, lng, lo);
+      if (p < end && !rl) {
+        const int64_t q = rsrc + (p - rbeg);
+        a.c_col[p] = __ldcs(a.ctil_col + q);
+        a.c_val[p] = __ldcs(a.ctil_val + q);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(512) k_copy_long(CopyArgs a) {
   const int64_t k = blockIdx.x;
   const int row = a.perm[a.long_first + k];
@@ -55,11 +92,16 @@ int sms() {
 
 cudaError_t launch_copy(const CopyArgs& a, int group, cudaStream_t s) {
   if (a.m > 0) {
-    const int64_t groups_per_block = 256 / group;
+    const int64_t groups_per_block = group > 0 ? 256 / group : 8;
     int64_t grid = (a.m + groups_per_block - 1) / groups_per_block;
     const int64_t cap = int64_t(sms()) * 16;
     if (grid > cap) grid = cap;
     switch (group) {
+      case 0: {
+        const int64_t g2 = ((a.m + 31) / 32 + 7) / 8;
+        k_copy_flat<<<(unsigned)(g2 < cap ? g2 : cap), 256, 0, s>>>(a);
+        break;
+      }
       case 4: k_copy<4><<<(unsigned)grid, 256, 0, s>>>(a); break;
       case 8: k_copy<8><<<(unsigned)grid, 256, 0, s>>>(a); break;
       case 16: k_copy<16><<<(unsigned)grid, 256, 0, s>>>(a); break;

@@ -22,6 +22,7 @@ def run(name, A, B=None, flags=0, reps=5):
     print("%-12s flags=%d ms=%.3f (all %s) GFlop/s=%.1f CB GB/s=%.1f nnzC=%d sum_u=%d stage_ms=%s tiers=%s long=%d growth=%d" % (
         name, flags, t, ["%.2f" % x for x in times], flops / t / 1e6, cb / t / 1e6, nnz, st["sum_u"],
         ["%.3f" % x for x in st["stage_ms"]], st["tier_rows"], st["long_rows"], st["growth_rounds"]), flush=True)
+    print("    classes:", {k: round(v["ms"], 3) for k, v in st["classes"].items()}, flush=True)
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c2"]
