@@ -314,84 +314,29 @@ __device__ __forceinline__ unsigned warp_insert(int* keys, int c, bool act, int&
   return h;
 }
 
-// Runtime-size variant (symbolic tables that grow): lg = log2 of the current size.
-__device__ __forceinline__ unsigned warp_insert_rt(int* keys, int c, bool act, int lg, int& inserted) {
-  const unsigned mask = (1u << lg) - 1;
-  unsigned h = ((unsigned)c * 0x9E3779B1u) >> (32 - lg);
-  int k = keys[h];
-  bool pend = act && k != c;
-  while (__any_sync(0xffffffffu, pend)) {
-    if (pend) {
-      if (k == kEmptyKey) {
-        const int old = atomicCAS(&keys[h], kEmptyKey, c);
-        if (old == kEmptyKey || old == c) {
-          inserted += old == kEmptyKey;
-          pend = false;
-        } else {
-          h = (h + 1) & mask;
-          k = keys[h];
-        }
-      } else if (k == c) {
-        pend = false;
-      } else {
-        h = (h + 1) & mask;
-        k = *(volatile int*)&keys[h];
-      }
-    }
-  }
-  return h;
-}
-
-// Double the table (keys only): move the keys to scratch, clear, reinsert.
-__device__ __forceinline__ void warp_grow(int* keys, int* scratch, int& lg, int lane) {
-  const int S = 1 << lg;
-  int n = 0;
-  for (int s0 = 0; s0 < S; s0 += 32) {
-    const int kk = keys[s0 + lane];
-    const bool occ = kk != kEmptyKey;
-    const unsigned bal = __ballot_sync(0xffffffffu, occ);
-    if (occ) scratch[n + __popc(bal & lanemask_lt())] = kk;
-    n += __popc(bal);
-  }
-  __syncwarp();
-  ++lg;
-  for (int s = lane; s < 2 * S; s += 32) keys[s] = kEmptyKey;
-  __syncwarp();
-  int dummy = 0;
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const bool act = i0 + lane < n;
-    warp_insert_rt(keys, act ? scratch[i0 + lane] : kEmptyKey, act, lg, dummy);
-  }
-  __syncwarp();
-}
-
 template <int LOG2S, int NW, int MODE>
 __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
   constexpr bool FILL = MODE == MODE_FILL;
   constexpr bool SORTED = MODE != MODE_COUNT;
   constexpr int S = 1 << LOG2S;
+  constexpr unsigned MASK = S - 1;
+  constexpr int SHIFT = 32 - LOG2S;
   __shared__ int s_keys[NW][S];
   __shared__ int s_scratch[SORTED ? NW : 1][SORTED ? S : 1];
   __shared__ double s_vals[FILL ? NW : 1][FILL ? S : 1];
   __shared__ WarpMeta<NW> meta;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int* keys = s_keys[w];
-  // symbolic modes start from a small table and double it when the load would pass 3/4
-  // (the count is not known yet: only the bound min(u_i, n) sized the class)
-  constexpr int LG0 = (MODE == MODE_STRUCT && LOG2S > 8) ? 8 : LOG2S;
-  int* gscratch = s_scratch[SORTED ? w : 0];
 
   for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    int lg = LG0;
 #pragma unroll 4
-    for (int s = lane; s < (1 << LG0); s += 32) {
+    for (int s = lane; s < S; s += 32) {
       keys[s] = kEmptyKey;
       if (FILL) s_vals[w][s] = -0.0;  // -0.0 + x == x: the first add is "c_ik <- value"
     }
-    int inserted = 0;  // per lane
-    int total = 0;     // warp-uniform (non-FILL modes)
+    int inserted = 0;
     for (int64_t e0 = a0; e0 < a1; e0 += 32) {
       const int nE = stage_a_chunk<NW, FILL>(a, meta, w, lane, e0, a1);
       int c0 = kEmptyKey, c1 = kEmptyKey;
@@ -412,34 +357,21 @@ __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
           if (FILL) v2 = __ldg(meta.pv[w][t + 2] + lane);
         }
         const int lt = meta.len[w][t];
+        const unsigned h = warp_insert<LOG2S>(keys, c0, lane < lt, inserted);  // lines 7-8
         if (FILL) {
-          const unsigned h = warp_insert<LOG2S>(keys, c0, lane < lt, inserted);  // lines 7-8
           __syncwarp();
           if (lane < lt) s_vals[w][h] = __dadd_rn(s_vals[w][h], __dmul_rn(meta.av[w][t], v0));
-        } else {
-          for (int q0 = 0; q0 < lt; q0 += 32) {
-            const int add = min(32, lt - q0);
-            if (4 * (total + add) > 3 * (1 << lg) && lg < LOG2S) {
-              do {
-                warp_grow(keys, gscratch, lg, lane);
-              } while (4 * (total + add) > 3 * (1 << lg) && lg < LOG2S);
-            }
-            const bool act = q0 + lane < lt;
-            const int c = q0 == 0 ? c0 : (act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey);
-            int nw = 0;
-            warp_insert_rt(keys, c, act, lg, nw);
-            inserted += nw;
-            total += __popc(__ballot_sync(0xffffffffu, nw != 0));
-          }
         }
-        if (FILL && lt > 32) {  // rest of a long b_j*, 32 columns per instruction
+        if (lt > 32) {  // rest of a long b_j*, 32 columns per instruction
           for (int q0 = 32; q0 < lt; q0 += 32) {
             const bool act = q0 + lane < lt;
             const int c = act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey;
             const unsigned hh = warp_insert<LOG2S>(keys, c, act, inserted);
-            const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
-            __syncwarp();
-            if (act) s_vals[w][hh] = __dadd_rn(s_vals[w][hh], __dmul_rn(meta.av[w][t], v));
+            if (FILL) {
+              const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
+              __syncwarp();
+              if (act) s_vals[w][hh] = __dadd_rn(s_vals[w][hh], __dmul_rn(meta.av[w][t], v));
+            }
           }
         }
         c0 = c1;
@@ -457,10 +389,10 @@ __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
       continue;
     }
     const int cnt = inserted;
-    int* scratch = gscratch;
+    int* scratch = s_scratch[SORTED ? w : 0];
     int base = 0;
 #pragma unroll 4
-    for (int s0 = 0; s0 < (1 << lg); s0 += 32) {
+    for (int s0 = 0; s0 < S; s0 += 32) {
       const int kk = keys[s0 + lane];
       const bool occ = kk != kEmptyKey;
       const unsigned bal = __ballot_sync(0xffffffffu, occ);
@@ -469,8 +401,8 @@ __global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
     }
     __syncwarp();
     const int64_t o = __ldg(a.out_off + row);
-    warp_emit_sorted<FILL>(keys, FILL ? s_vals[FILL ? w : 0] : nullptr, scratch, cnt, (1u << lg) - 1,
-                           32 - lg, lane, a.out_col + o, FILL ? a.out_val + o : nullptr);
+    warp_emit_sorted<FILL>(keys, FILL ? s_vals[FILL ? w : 0] : nullptr, scratch, cnt, MASK, SHIFT, lane,
+                           a.out_col + o, FILL ? a.out_val + o : nullptr);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
     __syncwarp();
   }
