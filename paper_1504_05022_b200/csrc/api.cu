@@ -6,6 +6,7 @@
 //            allocate C~ (hybrid) → stage 3 per class → long rows with the progressive
 //            growth loop ([P:297]) → scan of nnz(c_i*) → D2H of nnz(C) ([P:301]).
 // numeric:   stage 4 copy C~ → C (hybrid), or stage 3 again straight into C (PRECISE).
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -36,7 +37,7 @@ __global__ void k_iota(int32_t* p, int64_t n) {
 
 __global__ void k_long_slots(const LongState* st, int64_t n, int64_t* slots) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) slots[i] = 2 * st[i].cap;
+  if (i < n) slots[i] = long_table_slots(st[i].cap);
 }
 
 // PRECISE numeric: exact long-row tables (cap = nnz(c_i*) from the symbolic pass).
@@ -52,7 +53,7 @@ __global__ void k_long_exact(LongState* st, const int32_t* perm, int64_t first, 
   st[i].count = 0;
   st[i].next_a = arp[row];
   st[i].done = 0;
-  slots[i] = 2 * c;
+  slots[i] = long_table_slots(c);
 }
 
 __global__ void k_class_sums(int64_t m, const uint8_t* __restrict__ tier, const int64_t* __restrict__ U,
@@ -197,6 +198,26 @@ int env_int(const char* name, int def) {
   const char* v = getenv(name);
   return v ? atoi(v) : def;
 }
+
+// SPGEMM_TRACE=1: synchronise after each phase and print host wall times (debug only)
+struct Trace {
+  bool on;
+  cudaStream_t s;
+  const char* who;
+  std::chrono::steady_clock::time_point t0, last;
+  Trace(cudaStream_t st, const char* w) : on(getenv("SPGEMM_TRACE") != nullptr), s(st), who(w) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[spgemm %s] %-28s +%8.3f ms  (at %8.3f)\n", who, what,
+            std::chrono::duration<double, std::milli>(t - last).count(),
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    last = t;
+  }
+};
 
 // Allocate tables for the long rows listed in `list` (device, nlist entries) whose slot
 // counts are in h->lslots[0..nlist); assign pointers (moving the current ones to old_*).
@@ -433,6 +454,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   const int64_t m = h->m;
   const bool precise = (h->flags & SPGEMM_FLAG_PRECISE) != 0;
   const bool hybrid = !precise;
+  Trace tr(h->stream, "symbolic");
   cudaEventRecord(h->ev[0], h->stream);
   AL(h, &h->c_rp, m + 1);
   if (m == 0) {
@@ -469,9 +491,11 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   CK(h, launch_stage1(m, h->n, h->A, h->B.rp, tp, true, ws, h->stream));
   CK(h, launch_stage2(m, ws, true, h->n, h->stream));
   h->launches_sym = 3;
+  tr("alloc + stage 1-2");
   CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
   spgemm_status_t s = sync(h);
   if (s != SPGEMM_SUCCESS) return s;
+  tr("class counters D2H");
   for (int t = 0; t < NUM_TIERS; ++t) {
     h->tier_count[t] = h->pinned[kSumCount + t];
     h->tier_off[t] = h->pinned[kSumOff + t];
@@ -482,6 +506,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->max_u = h->pinned[kSumUMax];
   AL(h, &h->ctil_col, h->sum_cap);
   if (hybrid) AL(h, &h->ctil_val, h->sum_cap);
+  tr("C~ allocation");
   cudaEventRecord(h->ev[1], h->stream);
   // stage 3: one launch per non-empty class ([P:264] "only issue kernels for non-empty bins")
   for (int t = T_G1; t <= T_C8192; ++t) {
@@ -504,15 +529,32 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->tev_used[t] = true;
     ++h->launches_sym;
   }
+  tr("stage 3 classes");
   h->nlong = h->tier_count[T_LONG];
   h->long_first = h->tier_off[T_LONG];
   if (h->nlong > 0) cudaEventRecord(h->tev[T_LONG][0], h->stream);
-  s = run_long(h, hybrid ? MODE_FILL : MODE_COUNT);
-  if (s != SPGEMM_SUCCESS) return s;
+  if (hybrid) {
+    // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297]
+    s = run_long(h, MODE_FILL);
+    if (s != SPGEMM_SUCCESS) return s;
+    if (h->nlong > 0) h->launches_sym += 4 + 6 * h->growth_rounds;
+  } else if (h->nlong > 0) {
+    // precise: structure of long rows from a bitmap over the column window
+    Stage3Args a{};
+    a.A = h->A;
+    a.B = h->B;
+    a.n = h->n;
+    a.perm = ws.perm;
+    a.first = h->long_first;
+    a.count = h->nlong;
+    a.nnz_row = h->nnz_row;
+    a.mode = MODE_COUNT;
+    CK(h, launch_long_bitmap(a, h->stream));
+    h->launches_sym += 1;
+  }
   if (h->nlong > 0) {
     cudaEventRecord(h->tev[T_LONG][1], h->stream);
     h->tev_used[T_LONG] = true;
-    h->launches_sym += 4 + 6 * h->growth_rounds;
   }
   cudaEventRecord(h->ev[2], h->stream);
   // stage 4 (first half): sum the numbers of nonzero entries of all rows [P:301]
@@ -524,6 +566,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   s = sync(h);
   if (s != SPGEMM_SUCCESS) return s;
   h->nnz_c = h->pinned[0];
+  tr("long rows + scan + nnz D2H");
   if (precise) {
     // numeric classes from the exact row lengths (tables sized by nnz(c_i*), not the bound)
     CK(h, launch_rebin(m, h->n, h->nnz_row, tp, ws, h->stream));
@@ -538,11 +581,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->tier_off[NUM_TIERS] = h->pinned[kSumOff + NUM_TIERS];
     h->nlong = h->tier_count[T_LONG];
     h->long_first = h->tier_off[T_LONG];
-    if (h->nlong > 0) {
-      s = prepare_long_exact(h);
-      if (s != SPGEMM_SUCCESS) return s;
-      h->launches_sym += 7;
-    }
+    tr("re-binning");
   }
   h->sym_ok = true;
   *c_nnz = h->nnz_c;
@@ -601,29 +640,25 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         ++h->launches_num;
       }
       if (h->nlong > 0) {
-        LongArgs la{};
-        la.A = h->A;
-        la.B = h->B;
-        la.n = h->n;
-        la.perm = h->ws.perm;
-        la.first = h->long_first;
-        la.st = h->lst;
-        la.keys = h->lkeys;
-        la.vals = h->lvals;
-        la.old_keys = nullptr;
-        la.active = h->liota;
-        la.nactive = h->nlong;
-        la.overflow_list = h->lovf;
-        la.overflow_cnt = h->lovf_cnt;
-        la.nnz_row = nullptr;
-        la.mode = MODE_FILL;
+        Stage3Args a{};
+        a.A = h->A;
+        a.B = h->B;
+        a.n = h->n;
+        a.perm = h->ws.perm;
+        a.first = h->long_first;
+        a.count = h->nlong;
+        a.out_off = h->c_rp;
+        a.out_col = c_col_idx;
+        a.out_val = c_val;
+        a.mode = MODE_FILL;
         cudaEventRecord(h->tev[T_LONG][0], h->stream);
-        CK(h, launch_long(la, h->stream));
+        CK(h, launch_long_bitmap(a, h->stream));
         cudaEventRecord(h->tev[T_LONG][1], h->stream);
         h->tev_used[T_LONG] = true;
         ++h->launches_num;
       }
-      ca.m = 0;  // only the long rows are copied
+      ca.m = 0;     // nothing to copy: every row was written straight into C
+      ca.nlong = 0;
     }
     const double avg = double(h->nnz_c) / double(h->m);
     const int group = env_int("SPGEMM_COPY_GROUP", 0);  // 0 = flat warp copy (default)

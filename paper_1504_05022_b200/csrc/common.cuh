@@ -70,7 +70,7 @@ __host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
 __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
   if (t == T_EMPTY) return u == 0;
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
-  if (t >= T_W64 && t <= T_W2048) return 4 * (int64_t(64) << (t - T_W64)) >= 5 * nnz;
+  if (t >= T_W64 && t <= T_W2048) return (int64_t(64) << (t - T_W64)) >= 2 * nnz;  // dense: S >= 2·nnz
   if (t >= T_C2048 && t <= T_C8192) return nnz <= (int64_t(2048) << (t - T_C2048));
   return 1;
 }
@@ -164,6 +164,8 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
                          cudaStream_t s);
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
+// PRECISE long rows: bitmap over the column window (COUNT: nnz; FILL: ranks → C)
+cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s);
 
 // Exclusive scan of int64 values x[0..len) into y[0..len]; y[len] = total.  tmp must hold
 // scan_tmp_elems(len) int64.
@@ -181,6 +183,13 @@ struct LongState {
   int32_t done;
   int32_t pad;
 };
+// Slots of a long-row table of nominal capacity cap: a power of two >= 2·cap.
+__host__ __device__ inline int64_t long_table_slots(int64_t cap) {
+  int64_t s = 2;
+  while (s < 2 * cap) s <<= 1;
+  return s;
+}
+
 struct LongArgs {
   CsrView A, B;
   int64_t n;

@@ -9,9 +9,10 @@
 // results ... and continue the computation" [P:297].
 //
 // Here (a4/a5): one CTA per long row accumulates into an order-preserving
-// hash table in global memory with `cap` entries (2·cap slots).  Before each batch of a_ij
-// the CTA checks count + sum nnz(b_j*) <= cap (a safe bound on new entries); if not even
-// one a_ij fits it records the checkpoint (index of the next a_ij, [P:297]) and exits.
+// hash table in global memory with nominal capacity `cap` (2·cap slots).  A batch of a_ij is
+// taken only if its products fit the free slots (so it always completes); after a batch
+// whose distinct count passed `cap` — or if not even one a_ij fits — the CTA records the
+// checkpoint (index of the next a_ij, [P:297]) and exits.
 // The host grows cap to min(2·cap, min(u_i, n)) (never above the upper bound, reading Q8),
 // allocates the new tables and relaunches only the overflowed rows; the relaunched CTA
 // reloads the old table and resumes at the checkpoint.  At cap = min(u_i, n) no check is
@@ -71,11 +72,11 @@ __global__ void k_long_grow(LongState* st, const int32_t* __restrict__ list, int
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nlist) return;
   const int k = list[i];
-  old_slots[k] = 2 * st[k].cap;
+  old_slots[k] = long_table_slots(st[k].cap);
   int64_t c = st[k].cap * 2;                  // "we use 2x each time" [P:297]
   if (c > st[k].capmax) c = st[k].capmax;     // never above min(u_i, n) (reading Q8)
   st[k].cap = c;
-  slots_out[i] = 2 * c;
+  slots_out[i] = long_table_slots(c);
 }
 
 __global__ void k_long_assign(const int32_t* __restrict__ list, int64_t nlist,
@@ -125,13 +126,15 @@ __device__ __forceinline__ int64_t block_incl_scan64(int64_t v, int64_t* s_w, in
   return r;
 }
 
-__device__ __forceinline__ int64_t home_of(int c, int lo, double scale, int64_t H) {
+__device__ __forceinline__ int64_t home_of(int c, int lo, double scale, int64_t spread) {
   int64_t h = (int64_t)__dmul_rz((double)(c - lo), scale);  // monotone in c
-  return h < H - 1 ? h : H - 1;
+  return h < spread - 1 ? h : spread - 1;
 }
 
-// Insert key c into the global order-preserving table; returns its slot.
-__device__ __forceinline__ int64_t gt_insert(int32_t* keys, int c, int64_t h, int& isnew) {
+// Insert key c into the global order-preserving table of S slots; returns its slot.  A probe
+// run past the end wraps to slot 0 and flags the row (ordering then takes the robust path).
+__device__ __forceinline__ int64_t gt_insert(int32_t* keys, int c, int64_t h, int64_t S, int& isnew,
+                                             int& wrapped) {
   while (true) {
     const int k = __ldcg(keys + h);
     if (k == c) {
@@ -149,7 +152,10 @@ __device__ __forceinline__ int64_t gt_insert(int32_t* keys, int c, int64_t h, in
         return h;
       }
     }
-    ++h;
+    if (++h == S) {
+      h = 0;
+      wrapped = 1;
+    }
   }
 }
 
@@ -169,10 +175,14 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
   LongState st = a.st[k];
   int32_t* keys = a.keys[k];
   double* vals = fill ? a.vals[k] : nullptr;
-  const int64_t H = st.cap;
-  const int64_t S = 2 * H;
+  const int64_t S = long_table_slots(st.cap);
   const int64_t W = int64_t(st.hi) - st.lo + 1;
-  const double scale = W <= H ? 1.0 : (double)H / (double)W;
+  // homes spread over the table (load <= 1/2 keeps clusters short for scattered columns)
+  const int64_t spread = S - 64 > S / 2 ? S - 64 : S / 2;
+  const double scale = W <= spread ? 1.0 : (double)spread / (double)W;
+  __shared__ int s_slow;
+  if (threadIdx.x == 0) s_slow = 0;
+  int wrapped = 0;
 
   for (int64_t s = threadIdx.x; s < S; s += NT) {
     __stcg(keys + s, kEmptyKey);
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
       const int c = __ldcg(ok + s);
       if (c == kEmptyKey) continue;
       int isnew;
-      const int64_t h = gt_insert(keys, c, home_of(c, st.lo, scale, H), isnew);
+      const int64_t h = gt_insert(keys, c, home_of(c, st.lo, scale, spread), S, isnew, wrapped);
       if (fill) __stcg(vals + h, __ldcg(ov + s));
     }
     __syncthreads();
@@ -212,7 +222,9 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
     }
     int64_t tot;
     const int64_t inc = block_incl_scan64<NT>(len, s_w, &tot);
-    const int64_t budget = unbounded ? INT64_MAX : st.cap - count;
+    // physical safety: the table has 2·cap slots, so a batch whose products cannot exceed
+    // the free slots always completes; the nominal capacity (load 1/2) is checked after it
+    const int64_t budget = unbounded ? INT64_MAX : 2 * st.cap - count - 1;
     const int fits = (ee < a1) && inc <= budget;
     const int take = __syncthreads_count(fits);
     if (take == 0) {
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
       for (int q = lane; q < jl; q += 32) {
         const int c = __ldg(a.B.ci + jb + q);
         int isnew;
-        const int64_t h = gt_insert(keys, c, home_of(c, st.lo, scale, H), isnew);
+        const int64_t h = gt_insert(keys, c, home_of(c, st.lo, scale, spread), S, isnew, wrapped);
         ins += isnew;
         if (fill) atomicAdd(vals + h, __dmul_rn(at, __ldg(a.B.val + jb + q)));
       }
@@ -241,6 +253,10 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
     count += (int64_t)s_ins;
     e += take;
     __syncthreads();
+    if (!unbounded && count > st.cap && e < a1) {
+      overflow = true;  // over the nominal capacity: checkpoint here, grow 2x, resume ([P:297])
+      break;
+    }
   }
   if (overflow) {
     if (threadIdx.x == 0) {
@@ -258,31 +274,39 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
     if (a.nnz_row) a.nnz_row[row] = count;
   }
   if (!fill) return;
+  if (wrapped) s_slow = 1;
   __threadfence_block();
   __syncthreads();
-  // order clusters (maximal runs of occupied slots) by insertion sort
-  const int64_t chunk = (S + NT - 1) / NT;
-  const int64_t s0 = int64_t(threadIdx.x) * chunk;
-  const int64_t s1 = s0 + chunk < S ? s0 + chunk : S;
-  for (int64_t s = s0; s < s1; ++s) {
-    if (__ldcg(keys + s) == kEmptyKey || (s > 0 && __ldcg(keys + s - 1) != kEmptyKey)) continue;
-    int64_t end = s + 1;
-    while (end < S && __ldcg(keys + end) != kEmptyKey) ++end;
-    for (int64_t x = s + 1; x < end; ++x) {
-      const int kx = __ldcg(keys + x);
-      const double vx = __ldcg(vals + x);
-      int64_t y = x - 1;
-      while (y >= s && __ldcg(keys + y) > kx) {
-        __stcg(keys + y + 1, __ldcg(keys + y));
-        __stcg(vals + y + 1, __ldcg(vals + y));
-        --y;
+  if (!s_slow) {
+    // order clusters (maximal runs of occupied slots) by insertion sort; a wrapped table or a
+    // long cluster (clustered columns) sends the row to the robust path
+    const int64_t chunk = (S + NT - 1) / NT;
+    const int64_t s0 = int64_t(threadIdx.x) * chunk;
+    const int64_t s1 = s0 + chunk < S ? s0 + chunk : S;
+    for (int64_t s = s0; s < s1; ++s) {
+      if (__ldcg(keys + s) == kEmptyKey || (s > 0 && __ldcg(keys + s - 1) != kEmptyKey)) continue;
+      int64_t end = s + 1;
+      while (end < S && __ldcg(keys + end) != kEmptyKey && end - s <= 128) ++end;
+      if (end - s > 128) {
+        s_slow = 1;
+        break;
       }
-      __stcg(keys + y + 1, kx);
-      __stcg(vals + y + 1, vx);
+      for (int64_t x = s + 1; x < end; ++x) {
+        const int kx = __ldcg(keys + x);
+        const double vx = __ldcg(vals + x);
+        int64_t y = x - 1;
+        while (y >= s && __ldcg(keys + y) > kx) {
+          __stcg(keys + y + 1, __ldcg(keys + y));
+          __stcg(vals + y + 1, __ldcg(vals + y));
+          --y;
+        }
+        __stcg(keys + y + 1, kx);
+        __stcg(vals + y + 1, vx);
+      }
     }
+    __threadfence_block();
+    __syncthreads();
   }
-  __threadfence_block();
-  __syncthreads();
   // in-place ordered compaction to the front of the table
   int64_t base = 0;
   for (int64_t r0 = 0; r0 < S; r0 += NT) {
@@ -303,6 +327,33 @@ __global__ void __launch_bounds__(NT) k_long(LongArgs a) {
     base += tot;
     __threadfence_block();
     __syncthreads();
+  }
+  if (s_slow) {
+    // robust path: bitonic sort of the compacted (key, value) pairs in place
+    int64_t N = 1;
+    while (N < count) N <<= 1;
+    for (int64_t t = count + threadIdx.x; t < N && t < S; t += NT) __stcg(keys + t, INT_MAX);
+    __threadfence_block();
+    __syncthreads();
+    for (int64_t kk = 2; kk <= N; kk <<= 1) {
+      for (int64_t j = kk >> 1; j > 0; j >>= 1) {
+        for (int64_t i = threadIdx.x; i < (N >> 1); i += NT) {
+          const int64_t l0 = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          const int64_t l1 = l0 + j;
+          const bool asc = (l0 & kk) == 0;
+          const int k0 = __ldcg(keys + l0), k1 = __ldcg(keys + l1);
+          if ((k0 > k1) == asc) {
+            __stcg(keys + l0, k1);
+            __stcg(keys + l1, k0);
+            const double t0 = __ldcg(vals + l0);
+            __stcg(vals + l0, __ldcg(vals + l1));
+            __stcg(vals + l1, t0);
+          }
+        }
+        __threadfence_block();
+        __syncthreads();
+      }
+    }
   }
 }
 

@@ -1,0 +1,222 @@
+// longbm.cu — PRECISE strategy, long rows: a bitmap over the row's column window.
+//
+// The precise method ([P:165]) first computes the structure, then the values.  For rows too
+// long for a shared-memory hash (the paper's group 5, [P:222]) the structure of row i is
+// the set of columns hit by its products: one bit per column of the window [lo, hi] in
+// shared memory, processed in tiles of kTileBits columns.
+//   k_long_bm_count : per tile, set the bits of all products' columns (atomicOr), count them.
+//                     nnz(c_i*) = total popcount.  No hashing, no probing, no ordering.
+//   k_long_bm_fill  : per tile, rebuild the bits, exclusive prefix popcount per 32-bit word
+//                     → rank(c) = prefix[w] + popc(bits[w] & below(c)) is c's position in the
+//                     sorted row; write C's columns in order, zero the values, then add every
+//                     product into C.val[row_start + rank] (global fp64 atomics, order not
+//                     fixed: checked with the 1e-12·Σ|a||b| tolerance, R1).
+#include <climits>
+
+#include "common.cuh"
+
+namespace sg {
+
+namespace {
+
+constexpr int kBmNT = 512;
+constexpr int kTileWords = 16384;                 // 512 Ki columns per tile
+constexpr int64_t kTileBits = int64_t(kTileWords) * 32;
+constexpr size_t kBmSmem = size_t(kTileWords) * 8;  // bitmap + prefix (uint32 each)
+
+template <int NT>
+__device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int x = lane < NT / 32 ? s_w[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    if (lane < NT / 32) s_w[lane] = xi - x;
+    if (lane == 31) s_w[NT / 32] = xi;
+  }
+  __syncthreads();
+  const int ex = inc - v + s_w[w];
+  *total = s_w[NT / 32];
+  __syncthreads();
+  return ex;
+}
+
+// the row's column window: first / last column of every b_j*
+__device__ __forceinline__ void row_window(const Stage3Args& a, int64_t a0, int64_t a1, int* s_red,
+                                           int& lo, int& hi) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int l = INT_MAX, h = -1;
+  for (int64_t e = a0 + threadIdx.x; e < a1; e += blockDim.x) {
+    const int j = __ldg(a.A.ci + e);
+    const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
+    if (be > bs) {
+      l = min(l, __ldg(a.B.ci + bs));
+      h = max(h, __ldg(a.B.ci + be - 1));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
+    h = max(h, __shfl_xor_sync(0xffffffffu, h, o));
+  }
+  if (lane == 0) {
+    s_red[2 * w] = l;
+    s_red[2 * w + 1] = h;
+  }
+  __syncthreads();
+  lo = INT_MAX;
+  hi = -1;
+  for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
+    lo = min(lo, s_red[2 * k]);
+    hi = max(hi, s_red[2 * k + 1]);
+  }
+  __syncthreads();
+}
+
+// set the bits of every product column in [base, base + kTileBits)
+__device__ __forceinline__ void tile_mark(const Stage3Args& a, int64_t a0, int64_t a1, int64_t base,
+                                          unsigned* bm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x / 32;
+  for (int64_t e = a0 + w; e < a1; e += NW) {
+    const int j = __ldg(a.A.ci + e);
+    const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
+    for (int64_t q = jb + lane; q < je; q += 32) {
+      const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
+      if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* bm = reinterpret_cast<unsigned*>(smem);
+  __shared__ int s_red[2 * (kBmNT / 32)];
+  __shared__ unsigned long long s_cnt;
+  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int lo, hi;
+    row_window(a, a0, a1, s_red, lo, hi);
+    if (threadIdx.x == 0) s_cnt = 0;
+    for (int64_t base = lo; base <= hi; base += kTileBits) {
+      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
+      __syncthreads();
+      tile_mark(a, a0, a1, base, bm);
+      __syncthreads();
+      unsigned c = 0;
+      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) c += __popc(bm[k]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, (unsigned long long)c);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = (int64_t)s_cnt;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* bm = reinterpret_cast<unsigned*>(smem);
+  int* pre = reinterpret_cast<int*>(smem + size_t(kTileWords) * sizeof(unsigned));
+  __shared__ int s_red[2 * (kBmNT / 32)];
+  __shared__ int s_w[kBmNT / 32 + 1];
+  constexpr int WPT = kTileWords / kBmNT;  // words per thread in the prefix scan
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    const int64_t o = __ldg(a.out_off + row);
+    int lo, hi;
+    row_window(a, a0, a1, s_red, lo, hi);
+    int64_t done = 0;  // entries of the row already placed by earlier tiles
+    for (int64_t base = lo; base <= hi; base += kTileBits) {
+      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
+      __syncthreads();
+      tile_mark(a, a0, a1, base, bm);
+      __syncthreads();
+      // exclusive prefix popcount over the tile's words (thread t owns words [t·WPT, +WPT))
+      int loc = 0;
+#pragma unroll 4
+      for (int k = 0; k < WPT; ++k) loc += __popc(bm[threadIdx.x * WPT + k]);
+      int tot;
+      int run = block_excl_scan_i<kBmNT>(loc, &tot, s_w);
+#pragma unroll 4
+      for (int k = 0; k < WPT; ++k) {
+        const int wi = threadIdx.x * WPT + k;
+        const unsigned bits = bm[wi];
+        pre[wi] = run;
+        // C's columns of this tile, in order, and zeroed values
+        unsigned b = bits;
+        int p = run;
+        while (b) {
+          const int bit = __ffs(b) - 1;
+          b &= b - 1;
+          a.out_col[o + done + p] = (int)(base + int64_t(wi) * 32 + bit);
+          a.out_val[o + done + p] = 0.0;
+          ++p;
+        }
+        run += __popc(bits);
+      }
+      __threadfence();
+      __syncthreads();
+      // values: every product of a column in this tile adds into its rank (line 11)
+      for (int64_t e = a0 + w; e < a1; e += kBmNT / 32) {
+        const int j = __ldg(a.A.ci + e);
+        const double at = __ldg(a.A.val + e);
+        const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
+        for (int64_t q = jb + lane; q < je; q += 32) {
+          const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
+          if (d >= 0 && d < kTileBits) {
+            const int wi = (int)(d >> 5);
+            const unsigned below = (1u << (d & 31)) - 1u;
+            const int rank = pre[wi] + __popc(bm[wi] & below);
+            atomicAdd(a.out_val + o + done + rank, __dmul_rn(at, __ldg(a.B.val + q)));
+          }
+        }
+      }
+      done += tot;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace
+
+cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const bool fill = a.mode == MODE_FILL;
+  const size_t sm = fill ? kBmSmem : kBmSmem / 2;
+  auto kern = fill ? k_long_bm_fill : k_long_bm_count;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBmNT, sm);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = int64_t(sm_count()) * per_sm;
+  if (grid > a.count) grid = a.count;
+  kern<<<(unsigned)grid, kBmNT, sm, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sg

@@ -178,8 +178,9 @@ __device__ __forceinline__ int ht_find(const int* keys, int c, unsigned mask, in
   return (int)h;
 }
 
-// Sorted output of a warp table: compact the keys into `scratch`, sort them (registers for
-// N <= 128, shared memory above), then fetch each key's value from the intact table.
+// Sorted output of a warp table: the keys were compacted into `scratch`; sort them
+// (registers for N <= 128, shared memory above); with VALS fetch each key's value from the
+// intact table.
 template <int E, bool VALS>
 __device__ __forceinline__ void warp_emit_sorted_reg(const int* keys, const double* vals, const int* scratch,
                                                      int cnt, unsigned mask, int shift, int lane,
@@ -541,14 +542,16 @@ __device__ __forceinline__ int block_excl_scan_int(int v, int* total, int* s_w) 
 template <int LOG2H, int NT>
 __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
   constexpr int H = 1 << LOG2H;
-  constexpr int S = 2 * H;  // physical slots: probes never wrap (nnz <= cap <= H)
+  constexpr int S = 2 * H;       // physical slots (nnz <= H: load <= 1/2)
+  constexpr int SPREAD = S - 64;  // order-preserving homes cover [0, SPREAD)
   constexpr int NW = NT / 32;
+  constexpr int kLongCluster = 96;  // longer clusters: whole-row bitonic sort instead
   extern __shared__ __align__(16) unsigned char smem[];
   int* keys = reinterpret_cast<int*>(smem);
   double* vals = reinterpret_cast<double*>(smem + size_t(S) * sizeof(int));
   __shared__ int s_w[NW + 1];
   __shared__ int s_lo[NW], s_hi[NW];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_slow;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool fill = a.mode == MODE_FILL;
 
@@ -557,46 +560,55 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     // column window [lo, hi] of the row: first/last column of each b_j*
     int lo = INT_MAX, hi = -1;
-    for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
-      const int j = __ldg(a.A.ci + e);
-      const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
-      if (be > bs) {
-        lo = min(lo, __ldg(a.B.ci + bs));
-        hi = max(hi, __ldg(a.B.ci + be - 1));
+    if (fill) {
+      for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
+        const int j = __ldg(a.A.ci + e);
+        const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
+        if (be > bs) {
+          lo = min(lo, __ldg(a.B.ci + bs));
+          hi = max(hi, __ldg(a.B.ci + be - 1));
+        }
       }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) {
-      s_lo[w] = lo;
-      s_hi[w] = hi;
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lane == 0) {
+        s_lo[w] = lo;
+        s_hi[w] = hi;
+      }
     }
     for (int s = threadIdx.x; s < S; s += NT) {
       keys[s] = kEmptyKey;
       if (fill) vals[s] = 0.0;
     }
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    lo = s_lo[0];
-    hi = s_hi[0];
-    for (int k = 1; k < NW; ++k) {
-      lo = min(lo, s_lo[k]);
-      hi = max(hi, s_hi[k]);
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      s_slow = 0;
     }
-    const int64_t W = int64_t(hi) - lo + 1;
-    const float scale = W <= H ? 1.0f : (float)H / (float)W;
-    int inserted = 0;
+    __syncthreads();
+    float scale = 1.0f;
+    if (fill) {
+      lo = s_lo[0];
+      hi = s_hi[0];
+      for (int k = 1; k < NW; ++k) {
+        lo = min(lo, s_lo[k]);
+        hi = max(hi, s_hi[k]);
+      }
+      const int64_t W = int64_t(hi) - lo + 1;
+      scale = W <= SPREAD ? 1.0f : (float)SPREAD / (float)W;
+    }
+    int inserted = 0, wrapped = 0;
     for (int64_t e = a0 + w; e < a1; e += NW) {
       const int j = __ldg(a.A.ci + e);
       const double at = fill ? __ldg(a.A.val + e) : 0.0;
       const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
       for (int64_t q = jb + lane; q < je; q += 32) {
         const int c = __ldg(a.B.ci + q);
-        int h = (int)__fmul_rz((float)(c - lo), scale);   // monotone in c
-        h = h < H - 1 ? h : H - 1;
+        // FILL: order-preserving home (monotone in c); COUNT: any spread hash
+        int h = fill ? min((int)__fmul_rz((float)(c - lo), scale), SPREAD - 1)
+                     : (int)(((unsigned)c * 0x9E3779B1u) >> (32 - LOG2H - 1));
         volatile int* vk = keys;
         while (true) {
           const int k = vk[h];
@@ -609,14 +621,23 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
             }
             if (old == c) break;
           }
-          ++h;
+          if (++h == S) {
+            h = 0;
+            wrapped = 1;
+          }
         }
         if (fill) atomicAdd(&vals[h], __dmul_rn(at, __ldg(a.B.val + q)));
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
-    if (lane == 0) atomicAdd(&s_cnt, inserted);
+    for (int o = 16; o > 0; o >>= 1) {
+      inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+      wrapped |= __shfl_xor_sync(0xffffffffu, wrapped, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&s_cnt, inserted);
+      if (wrapped) s_slow = 1;
+    }
     __syncthreads();
     const int nnz = s_cnt;
     if (!fill) {
@@ -624,38 +645,90 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
       __syncthreads();
       continue;
     }
-    // order each cluster (maximal run of occupied slots) by insertion sort
-    constexpr int CH = S / NT;
-    for (int s = threadIdx.x * CH; s < (threadIdx.x + 1) * CH; ++s) {
-      if (keys[s] == kEmptyKey || (s > 0 && keys[s - 1] != kEmptyKey)) continue;
-      int end = s + 1;
-      while (end < S && keys[end] != kEmptyKey) ++end;
-      for (int x = s + 1; x < end; ++x) {
-        const int kx = keys[x];
-        const double vx = vals[x];
-        int y = x - 1;
-        while (y >= s && keys[y] > kx) {
-          keys[y + 1] = keys[y];
-          vals[y + 1] = vals[y];
-          --y;
-        }
-        keys[y + 1] = kx;
-        vals[y + 1] = vx;
-      }
-    }
-    __syncthreads();
     const int64_t o = __ldg(a.out_off + row);
-    int base = 0;
-    for (int s0 = 0; s0 < S; s0 += NT) {
-      const int s = s0 + threadIdx.x;
-      const bool occ = keys[s] != kEmptyKey;
-      int tot;
-      const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);
-      if (occ) {
-        a.out_col[o + base + pos] = keys[s];
-        a.out_val[o + base + pos] = vals[s];
+    if (!s_slow) {
+      // order each cluster (maximal run of occupied slots) by insertion sort; a long
+      // cluster (clustered columns) switches the row to the bitonic path below
+      constexpr int CH = S / NT;
+      for (int s = threadIdx.x * CH; s < (threadIdx.x + 1) * CH; ++s) {
+        if (keys[s] == kEmptyKey || (s > 0 && keys[s - 1] != kEmptyKey)) continue;
+        int end = s + 1;
+        while (end < S && keys[end] != kEmptyKey && end - s <= kLongCluster) ++end;
+        if (end - s > kLongCluster) {
+          s_slow = 1;
+          break;
+        }
+        for (int x = s + 1; x < end; ++x) {
+          const int kx = keys[x];
+          const double vx = vals[x];
+          int y = x - 1;
+          while (y >= s && keys[y] > kx) {
+            keys[y + 1] = keys[y];
+            vals[y + 1] = vals[y];
+            --y;
+          }
+          keys[y + 1] = kx;
+          vals[y + 1] = vx;
+        }
       }
-      base += tot;
+      __syncthreads();
+    }
+    if (!s_slow) {
+      int base = 0;
+      for (int s0 = 0; s0 < S; s0 += NT) {
+        const int s = s0 + threadIdx.x;
+        const bool occ = keys[s] != kEmptyKey;
+        int tot;
+        const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);
+        if (occ) {
+          a.out_col[o + base + pos] = keys[s];
+          a.out_val[o + base + pos] = vals[s];
+        }
+        base += tot;
+      }
+    } else {
+      // robust path: compact (key, value) pairs to the front, bitonic sort by key, write
+      int base = 0;
+      for (int s0 = 0; s0 < S; s0 += NT) {
+        const int s = s0 + threadIdx.x;
+        const int k = keys[s];
+        const double v = vals[s];
+        const bool occ = k != kEmptyKey;
+        int tot;
+        const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);  // has __syncthreads
+        if (occ) {
+          keys[base + pos] = k;
+          vals[base + pos] = v;
+        }
+        base += tot;
+        __syncthreads();
+      }
+      int N = 1;
+      while (N < nnz) N <<= 1;
+      for (int s = nnz + threadIdx.x; s < N; s += NT) keys[s] = INT_MAX;
+      __syncthreads();
+      for (int kk = 2; kk <= N; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < (N >> 1); i += NT) {
+            const int l0 = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+            const int l1 = l0 + j;
+            const bool asc = (l0 & kk) == 0;
+            const int k0 = keys[l0], k1 = keys[l1];
+            if ((k0 > k1) == asc) {
+              keys[l0] = k1;
+              keys[l1] = k0;
+              const double t = vals[l0];
+              vals[l0] = vals[l1];
+              vals[l1] = t;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int t = threadIdx.x; t < nnz; t += NT) {
+        a.out_col[o + t] = keys[t];
+        a.out_val[o + t] = vals[t];
+      }
     }
     if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncthreads();
