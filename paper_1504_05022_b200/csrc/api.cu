@@ -21,6 +21,15 @@ using namespace sg;
 namespace {
 
 thread_local std::string t_last_error;
+// Host-side per-thread resources reused across handles (creating them per handle put
+// cudaMallocHost / cudaFreeHost and ~40 event creations inside every multiply).
+thread_local int64_t* t_pinned = nullptr;  // small pinned scratch for the counter read-backs
+struct EventSet {
+  int device;
+  cudaEvent_t ev[6];
+  cudaEvent_t tev[NUM_TIERS][2];
+};
+thread_local std::vector<EventSet*> t_event_pool;
 int g_force_tier = -1;
 int64_t g_long_cap0 = 16384;
 int64_t g_long_threshold = 0;
@@ -118,8 +127,9 @@ struct spgemm_handle_s {
   bool sym_ok = false;
   int64_t nnz_c = 0;
   std::string err;
-  cudaEvent_t ev[6] = {};
-  cudaEvent_t tev[NUM_TIERS][2] = {};
+  EventSet* evs = nullptr;
+  cudaEvent_t* ev = nullptr;
+  cudaEvent_t (*tev)[2] = nullptr;
   bool tev_used[NUM_TIERS] = {};
   int32_t launches_sym = 0, launches_num = 0;
   bool ev_ok = false;
@@ -406,21 +416,42 @@ spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int
   h->b_nnz = b_nnz;
   h->A = CsrView{a_row_ptr, a_col_idx, a_val};
   h->B = CsrView{b_row_ptr, b_col_idx, b_val};
-  // keep freed workspace cached in the stream-ordered pool (warm allocations)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  // keep freed workspace cached in the stream-ordered pool (warm allocations); once per device
+  static thread_local uint64_t pool_done = 0;
+  if (h->device < 64 && !(pool_done & (1ull << h->device))) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_done |= 1ull << h->device;
   }
-  cudaError_t e = cudaMallocHost(&h->pinned, sizeof(int64_t) * (kSumLen + 8));
-  if (e != cudaSuccess) {
-    spgemm_status_t s = cuda_fail(nullptr, e, "cudaMallocHost");
-    delete h;
-    return s;
+  cudaError_t e = cudaSuccess;
+  if (!t_pinned) {
+    e = cudaMallocHost(&t_pinned, sizeof(int64_t) * (kSumLen + 8));
+    if (e != cudaSuccess) {
+      t_pinned = nullptr;
+      spgemm_status_t s = cuda_fail(nullptr, e, "cudaMallocHost");
+      delete h;
+      return s;
+    }
   }
-  for (int i = 0; i < 6; ++i) cudaEventCreate(&h->ev[i]);
-  for (int t = 0; t < NUM_TIERS; ++t)
-    for (int i = 0; i < 2; ++i) cudaEventCreate(&h->tev[t][i]);
+  h->pinned = t_pinned;
+  for (size_t i = 0; i < t_event_pool.size(); ++i)
+    if (t_event_pool[i]->device == h->device) {
+      h->evs = t_event_pool[i];
+      t_event_pool.erase(t_event_pool.begin() + i);
+      break;
+    }
+  if (!h->evs) {
+    h->evs = new EventSet();
+    h->evs->device = h->device;
+    for (int i = 0; i < 6; ++i) cudaEventCreate(&h->evs->ev[i]);
+    for (int t = 0; t < NUM_TIERS; ++t)
+      for (int i = 0; i < 2; ++i) cudaEventCreate(&h->evs->tev[t][i]);
+  }
+  h->ev = h->evs->ev;
+  h->tev = h->evs->tev;
   h->ev_ok = true;
   if (flags & SPGEMM_FLAG_VALIDATE) {
     int32_t* err = nullptr;
@@ -677,12 +708,7 @@ spgemm_status_t spgemm_destroy(spgemm_handle_t h) {
   cudaSetDevice(h->device);
   free_symbolic(h);
   cudaStreamSynchronize(h->stream);
-  if (h->pinned) cudaFreeHost(h->pinned);
-  if (h->ev_ok) {
-    for (int i = 0; i < 6; ++i) cudaEventDestroy(h->ev[i]);
-    for (int t = 0; t < NUM_TIERS; ++t)
-      for (int i = 0; i < 2; ++i) cudaEventDestroy(h->tev[t][i]);
-  }
+  if (h->evs) t_event_pool.push_back(h->evs);  // reused by the next handle of this thread
   delete h;
   return SPGEMM_SUCCESS;
 }

@@ -90,10 +90,13 @@ def test_c4_full(smoothed):
         _check_sampled(AP, A, P, _samples(A.shape[0], width=32), exact=True)
 
 
-def test_c3b_full():
-    """Graph500-skew R-MAT at scale 18 (heavy tail; long rows on the progressive path)."""
+@pytest.mark.parametrize("strategy", ["hybrid", "precise"])
+def test_c3b_full(strategy):
+    """Graph500-skew R-MAT at scale 18 (heavy tail; long rows on the progressive path in
+    hybrid, on the bitmap path in precise)."""
+    import paper_1504_05022_b200 as sg
     A = gen.rmat(18, 16, (0.57, 0.19, 0.19, 0.05), seed=gen.SEED, mode="int")
-    C, nnz, st = _run(A)
+    C, nnz, st = _run(A, flags=sg.FLAG_PRECISE if strategy == "precise" else 0)
     assert st["long_rows"] > 0
     u, tot = oracle.upper_bound(A, A)
     assert st["sum_u"] == tot

@@ -121,6 +121,19 @@ def test_forced_tier(tier):
     compare(g, R, exact=True, what="tier %d" % tier)
 
 
+@pytest.mark.parametrize("tier", [3, 6, 7, 9, 11, 12, 13, 15, 16])
+def test_forced_tier_precise(tier):
+    """PRECISE strategy: symbolic (structure) and numeric (dense / bitmap) classes agree
+    with the oracle when rows are forced through each class."""
+    import paper_1504_05022_b200 as sg
+    us = [2, 3, 7, 16, 30, 32, 40, 100, 300, 700, 1500, 3000, 6000]
+    A, B = gen.forced_u_pair(us, n=9000, seed=tier + 50, mode="int", dup=0.5)
+    sg.set_debug(tier, 0, 0)
+    g = run_gpu(A, B, flags=sg.FLAG_PRECISE)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True, what="precise tier %d" % tier)
+
+
 @pytest.mark.parametrize("u", [600, 1500, 5000])
 @pytest.mark.parametrize("dup", [0.0, 0.5, 0.95])
 def test_long_growth(u, dup):
@@ -134,7 +147,8 @@ def test_long_growth(u, dup):
     R = oracle.spgemm(A, B)
     compare(g, R, exact=True, what="u=%d dup=%s" % (u, dup))
     assert g["stats"]["long_rows"] == 4
-    assert g["stats"]["growth_rounds"] >= 1
+    if int(np.diff(R.rp).max()) > 64:  # some row outgrew the initial capacity: re-allocation ran
+        assert g["stats"]["growth_rounds"] >= 1
 
 
 @pytest.mark.parametrize("flags_name", ["PRECISE", "UPPER_BOUND"])
