@@ -540,7 +540,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   tr("C~ allocation");
   cudaEventRecord(h->ev[1], h->stream);
   // stage 3: one launch per non-empty class ([P:264] "only issue kernels for non-empty bins")
-  for (int t = T_G1; t <= T_C8192; ++t) {
+  for (int t = T_G1; t < T_LONG; ++t) {
     if (h->tier_count[t] == 0) continue;
     Stage3Args a{};
     a.A = h->A;
@@ -647,7 +647,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
     ca.c_val = c_val;
     if (precise) {
       // stage 3 again, values on, straight into C at its final offsets
-      for (int t = T_G1; t <= T_C8192; ++t) {
+      for (int t = T_G1; t < T_LONG; ++t) {
         if (h->tier_count[t] == 0) continue;
         Stage3Args a{};
         a.A = h->A;

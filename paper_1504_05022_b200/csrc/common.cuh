@@ -11,6 +11,9 @@
 //                                                 (slot of the bitonic-ESC group 4)
 //   T_C2048..T_C8192   cap <= H                   one CTA per row, order-preserving hash with
 //                                                 H home slots in 2H smem slots
+//   T_E2048..T_E8192   u <= U (cap > 1638)        one CTA per row, bucket ESC: products counting-
+//                                                 sorted into buckets (monotone bucket function),
+//                                                 each bucket sorted by (column, product index)
 //   T_LONG             otherwise                  progressive global table + re-allocation
 //                                                 (group 5, [P:286-297])
 #pragma once
@@ -26,8 +29,9 @@ enum Tier : int {
   T_G1 = 1, T_G2 = 2, T_G4 = 3, T_G8 = 4, T_G16 = 5, T_G32 = 6,
   T_W64 = 7, T_W128 = 8, T_W256 = 9, T_W512 = 10, T_W1024 = 11, T_W2048 = 12,
   T_C2048 = 13, T_C4096 = 14, T_C8192 = 15,
-  T_LONG = 16,
-  NUM_TIERS = 17
+  T_E2048 = 16, T_E4096 = 17, T_E8192 = 18,
+  T_LONG = 19,
+  NUM_TIERS = 20
 };
 static_assert(NUM_TIERS == SPGEMM_NUM_TIERS, "tier count mismatch with the ABI header");
 
@@ -46,7 +50,14 @@ __host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap) {
     return 4 * S >= 5 * cap;
   }
   if (t >= T_C2048 && t <= T_C8192) return cap <= (int64_t(2048) << (t - T_C2048));
+  if (t >= T_E2048 && t <= T_E8192) return u <= (int64_t(2048) << (t - T_E2048));
   return 1;  // T_LONG holds anything
+}
+
+__host__ __device__ inline int esc_class(int64_t u) {
+  for (int t = T_E2048; t <= T_E8192; ++t)
+    if (u <= (int64_t(2048) << (t - T_E2048))) return t;
+  return -1;
 }
 
 // Stage-2 classification of one row (the B200 re-derivation of Algorithm 3 [P:226-260]).
@@ -60,7 +71,11 @@ __host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
     while ((int64_t(1) << g) < u) ++g;
     return T_G1 + g;
   }
-  for (int t = T_W64; t <= T_C8192; ++t)
+  for (int t = T_W64; t <= T_W2048; ++t)
+    if (tier_capacity_ok(t, u, cap)) return t;
+  const int e = esc_class(u);  // products fit one CTA's shared memory: bucket ESC
+  if (e >= 0) return e;
+  for (int t = T_C2048; t <= T_C8192; ++t)
     if (tier_capacity_ok(t, u, cap)) return t;
   return T_LONG;
 }
@@ -72,6 +87,7 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
   if (t >= T_W64 && t <= T_W2048) return (int64_t(64) << (t - T_W64)) >= 2 * nnz;  // dense: S >= 2·nnz
   if (t >= T_C2048 && t <= T_C8192) return nnz <= (int64_t(2048) << (t - T_C2048));
+  if (t >= T_E2048 && t <= T_E8192) return u <= (int64_t(2048) << (t - T_E2048));
   return 1;
 }
 
@@ -93,6 +109,8 @@ __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_cl
   if (has_struct)
     for (int t = T_W64; t <= T_W2048; ++t)
       if ((int64_t(64) << (t - T_W64)) >= 2 * nnz) return t;
+  const int e = esc_class(u);
+  if (e >= 0) return e;
   for (int t = T_C2048; t <= T_C8192; ++t)
     if (nnz <= (int64_t(2048) << (t - T_C2048))) return t;
   return T_LONG;
@@ -164,6 +182,8 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
                          cudaStream_t s);
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
+// bucket-ESC classes (esc.cu)
+cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s);
 // PRECISE long rows: bitmap over the column window (COUNT: nnz; FILL: ranks → C)
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s);
 

@@ -20,9 +20,10 @@ namespace sg {
 namespace {
 
 constexpr int kBmNT = 512;
-constexpr int kTileWords = 16384;                 // 512 Ki columns per tile
+constexpr int kTileWords = 8192;                  // 256 Ki columns per tile (64 KB with prefix)
+constexpr int kChunk = 256;                       // products per work item (load balance)
 constexpr int64_t kTileBits = int64_t(kTileWords) * 32;
-constexpr size_t kBmSmem = size_t(kTileWords) * 8;  // bitmap + prefix (uint32 each)
+constexpr size_t kBmSmem = size_t(kTileWords) * 6;  // bitmap + one prefix per word pair
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
@@ -85,17 +86,51 @@ __device__ __forceinline__ void row_window(const Stage3Args& a, int64_t a0, int6
   __syncthreads();
 }
 
-// set the bits of every product column in [base, base + kTileBits)
-__device__ __forceinline__ void tile_mark(const Stage3Args& a, int64_t a0, int64_t a1, int64_t base,
-                                          unsigned* bm) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x / 32;
-  for (int64_t e = a0 + w; e < a1; e += NW) {
-    const int j = __ldg(a.A.ci + e);
-    const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
-    for (int64_t q = jb + lane; q < je; q += 32) {
-      const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-      if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+// Visit every product of row [a0, a1) with a balanced schedule: a_ij are taken NT at a time,
+// each b_j* is cut into kChunk-product work items, and warps take work items round-robin
+// (hub rows of B no longer leave the other warps of the CTA waiting at the barrier).
+struct BmBatch {
+  long long bs[kBmNT];
+  int len[kBmNT];
+  int cinc[kBmNT];  // inclusive scan of work items per a_ij
+  double av[kBmNT];
+};
+
+template <bool VALS, typename F>
+__device__ __forceinline__ void for_each_product(const Stage3Args& a, int64_t a0, int64_t a1, BmBatch& sb,
+                                                 int* s_w, F&& f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = kBmNT / 32;
+  for (int64_t e0 = a0; e0 < a1; e0 += kBmNT) {
+    const int64_t e = e0 + threadIdx.x;
+    int len = 0;
+    if (e < a1) {
+      const int j = __ldg(a.A.ci + e);
+      const int64_t bs = __ldg(a.B.rp + j);
+      len = (int)(__ldg(a.B.rp + j + 1) - bs);
+      sb.bs[threadIdx.x] = bs;
+      sb.len[threadIdx.x] = len;
+      if (VALS) sb.av[threadIdx.x] = __ldg(a.A.val + e);
     }
+    const int nch = (len + kChunk - 1) / kChunk;
+    int tot;
+    const int ex = block_excl_scan_i<kBmNT>(nch, &tot, s_w);
+    sb.cinc[threadIdx.x] = ex + nch;
+    __syncthreads();
+    for (int item = w; item < tot; item += NW) {
+      int lo = 0, hi = kBmNT - 1;  // first t with cinc[t] > item
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sb.cinc[mid] > item) hi = mid;
+        else lo = mid + 1;
+      }
+      const int t = lo;
+      const int first_item = sb.cinc[t] - (sb.len[t] + kChunk - 1) / kChunk;
+      const int64_t q0 = sb.bs[t] + int64_t(item - first_item) * kChunk;
+      const int64_t qe = min(q0 + kChunk, (int64_t)sb.bs[t] + sb.len[t]);
+      const double at = VALS ? sb.av[t] : 0.0;
+      for (int64_t q = q0 + lane; q < qe; q += 32) f(q, at);
+    }
+    __syncthreads();
   }
 }
 
@@ -103,6 +138,8 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
   __shared__ int s_red[2 * (kBmNT / 32)];
+  __shared__ int s_w[kBmNT / 32 + 1];
+  __shared__ BmBatch sb;
   __shared__ unsigned long long s_cnt;
   for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
     const int row = __ldg(a.perm + a.first + r);
@@ -113,8 +150,10 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
     for (int64_t base = lo; base <= hi; base += kTileBits) {
       for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
       __syncthreads();
-      tile_mark(a, a0, a1, base, bm);
-      __syncthreads();
+      for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
+        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
+        if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+      });
       unsigned c = 0;
       for (int k = threadIdx.x; k < kTileWords; k += kBmNT) c += __popc(bm[k]);
 #pragma unroll
@@ -133,8 +172,8 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
   int* pre = reinterpret_cast<int*>(smem + size_t(kTileWords) * sizeof(unsigned));
   __shared__ int s_red[2 * (kBmNT / 32)];
   __shared__ int s_w[kBmNT / 32 + 1];
+  __shared__ BmBatch sb;
   constexpr int WPT = kTileWords / kBmNT;  // words per thread in the prefix scan
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
@@ -145,8 +184,10 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
     for (int64_t base = lo; base <= hi; base += kTileBits) {
       for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
       __syncthreads();
-      tile_mark(a, a0, a1, base, bm);
-      __syncthreads();
+      for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
+        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
+        if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+      });
       // exclusive prefix popcount over the tile's words (thread t owns words [t·WPT, +WPT))
       int loc = 0;
 #pragma unroll 4
@@ -157,7 +198,7 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
       for (int k = 0; k < WPT; ++k) {
         const int wi = threadIdx.x * WPT + k;
         const unsigned bits = bm[wi];
-        pre[wi] = run;
+        if ((wi & 1) == 0) pre[wi >> 1] = run;
         // C's columns of this tile, in order, and zeroed values
         unsigned b = bits;
         int p = run;
@@ -173,20 +214,15 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
       __threadfence();
       __syncthreads();
       // values: every product of a column in this tile adds into its rank (line 11)
-      for (int64_t e = a0 + w; e < a1; e += kBmNT / 32) {
-        const int j = __ldg(a.A.ci + e);
-        const double at = __ldg(a.A.val + e);
-        const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
-        for (int64_t q = jb + lane; q < je; q += 32) {
-          const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-          if (d >= 0 && d < kTileBits) {
-            const int wi = (int)(d >> 5);
-            const unsigned below = (1u << (d & 31)) - 1u;
-            const int rank = pre[wi] + __popc(bm[wi] & below);
-            atomicAdd(a.out_val + o + done + rank, __dmul_rn(at, __ldg(a.B.val + q)));
-          }
+      for_each_product<true>(a, a0, a1, sb, s_w, [&](int64_t q, double at) {
+        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
+        if (d >= 0 && d < kTileBits) {
+          const int wi = (int)(d >> 5);
+          const unsigned below = (1u << (d & 31)) - 1u;
+          const int rank = pre[wi >> 1] + ((wi & 1) ? __popc(bm[wi - 1]) : 0) + __popc(bm[wi] & below);
+          atomicAdd(a.out_val + o + done + rank, __dmul_rn(at, __ldg(a.B.val + q)));
         }
-      }
+      });
       done += tot;
       __syncthreads();
     }
@@ -206,7 +242,7 @@ int sm_count() {
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const bool fill = a.mode == MODE_FILL;
-  const size_t sm = fill ? kBmSmem : kBmSmem / 2;
+  const size_t sm = fill ? kBmSmem : size_t(kTileWords) * sizeof(unsigned);
   auto kern = fill ? k_long_bm_fill : k_long_bm_count;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

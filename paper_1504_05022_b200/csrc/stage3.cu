@@ -34,7 +34,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // --------------------------------------------------------------- G-lane sort groups
-template <int G, int NT>
+template <int G, int NT, bool KEY32>
 __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
   __shared__ int s_col[NT];
@@ -101,19 +101,47 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
       }
       cnt += tot;
     }
-    // bitonic sort of (column, product index) across the G lanes of the group
-#pragma unroll
-    for (int k = 2; k <= G; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const unsigned long long p = __shfl_xor_sync(0xffffffffu, key, j);
-        const bool up = (gl & k) == 0, lower = (gl & j) == 0;
-        key = (lower == up) ? (key < p ? key : p) : (key > p ? key : p);
-      }
+    if (!fill) {
+      // count only: distinct columns of the group = leaders of equal-key lane sets
+      const unsigned long long gk = key == ~0ull ? ~0ull - lane : ((unsigned long long)(lane / G) << 32) | (key >> 32);
+      const unsigned same = __match_any_sync(0xffffffffu, gk);
+      const bool lead = key != ~0ull && (__ffs(same) - 1) == lane;
+      const int nnz = __popc(__ballot_sync(0xffffffffu, lead) & gbits);
+      if (has && gl == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+      continue;
     }
-    const bool valid = key != ~0ull;
-    const int col = valid ? (int)(key >> 32) : -1;
-    const int src = (int)(key & 31u);
+    // bitonic sort of (column, product index) across the G lanes of the group; columns below
+    // 2^27 pack with the 5-bit product index into one 32-bit key
+    int col, src;
+    bool valid;
+    if (KEY32) {
+      unsigned k32 = key == ~0ull ? 0xffffffffu : ((unsigned)(key >> 32) << 5) | (unsigned)gl;
+#pragma unroll
+      for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const unsigned p = __shfl_xor_sync(0xffffffffu, k32, j);
+          const bool up = (gl & k) == 0, lower = (gl & j) == 0;
+          k32 = (lower == up) ? min(k32, p) : max(k32, p);
+        }
+      }
+      valid = k32 != 0xffffffffu;
+      col = valid ? (int)(k32 >> 5) : -1;
+      src = (int)(k32 & 31u);
+    } else {
+#pragma unroll
+      for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const unsigned long long p = __shfl_xor_sync(0xffffffffu, key, j);
+          const bool up = (gl & k) == 0, lower = (gl & j) == 0;
+          key = (lower == up) ? (key < p ? key : p) : (key > p ? key : p);
+        }
+      }
+      valid = key != ~0ull;
+      col = valid ? (int)(key >> 32) : -1;
+      src = (int)(key & 31u);
+    }
     const double v = __shfl_sync(0xffffffffu, myv, valid ? src : gl, G);
     const int prev = __shfl_up_sync(0xffffffffu, col, 1, G);
     const bool head = valid && (gl == 0 || prev != col);
@@ -674,17 +702,21 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
       __syncthreads();
     }
     if (!s_slow) {
-      int base = 0;
-      for (int s0 = 0; s0 < S; s0 += NT) {
-        const int s = s0 + threadIdx.x;
-        const bool occ = keys[s] != kEmptyKey;
-        int tot;
-        const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);
-        if (occ) {
-          a.out_col[o + base + pos] = keys[s];
-          a.out_val[o + base + pos] = vals[s];
+      // ordered compaction: each thread owns CH consecutive slots; one block scan of counts
+      constexpr int CH = S / NT;
+      const int s0 = threadIdx.x * CH;
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) cnt += keys[s0 + k] != kEmptyKey;
+      int tot;
+      int pos = block_excl_scan_int<NT>(cnt, &tot, s_w);
+      for (int k = 0; k < CH; ++k) {
+        const int kk = keys[s0 + k];
+        if (kk != kEmptyKey) {
+          a.out_col[o + pos] = kk;
+          a.out_val[o + pos] = vals[s0 + k];
+          ++pos;
         }
-        base += tot;
       }
     } else {
       // robust path: compact (key, value) pairs to the front, bitonic sort by key, write
@@ -774,12 +806,16 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   const bool fill = a.mode == MODE_FILL || a.mode == MODE_DENSE;
   const size_t per_slot = fill ? 12 : 4;
   switch (tier) {
-    case T_G1: return launch_persistent(k_group<1, 256>, 256, 0, a.count, 256, a, s);
-    case T_G2: return launch_persistent(k_group<2, 256>, 256, 0, a.count, 128, a, s);
-    case T_G4: return launch_persistent(k_group<4, 256>, 256, 0, a.count, 64, a, s);
-    case T_G8: return launch_persistent(k_group<8, 256>, 256, 0, a.count, 32, a, s);
-    case T_G16: return launch_persistent(k_group<16, 256>, 256, 0, a.count, 16, a, s);
-    case T_G32: return launch_persistent(k_group<32, 256>, 256, 0, a.count, 8, a, s);
+#define SG_GROUP(G, UPB)                                                                      \
+  return a.n <= (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true>, 256, 0, a.count, UPB, a, s) \
+                                   : launch_persistent(k_group<G, 256, false>, 256, 0, a.count, UPB, a, s)
+    case T_G1: SG_GROUP(1, 256);
+    case T_G2: SG_GROUP(2, 128);
+    case T_G4: SG_GROUP(4, 64);
+    case T_G8: SG_GROUP(8, 32);
+    case T_G16: SG_GROUP(16, 16);
+    case T_G32: SG_GROUP(32, 8);
+#undef SG_GROUP
     case T_W64:
       if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<6, 8>, 256, 0, a.count, 8, a, s);
       if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<6, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
@@ -810,6 +846,9 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
       if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<11, 1, MODE_FILL>, 32, 0, a.count, 1, a, s);
       if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<11, 2, MODE_STRUCT>, 64, 0, a.count, 2, a, s);
       return launch_persistent(k_warp_hash<11, 4, MODE_COUNT>, 128, 0, a.count, 4, a, s);
+    case T_E2048:
+    case T_E4096:
+    case T_E8192: return launch_esc(tier, a, s);
     case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
     case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
     case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);

@@ -88,10 +88,13 @@ def _classify(u, n):
     for t in range(7, 13):
         if 4 * (64 << (t - 7)) >= 5 * cap:
             return t
+    for t in range(16, 19):          # bucket-ESC classes by the product count u
+        if u <= (2048 << (t - 16)):
+            return t
     for t in range(13, 16):
         if cap <= (2048 << (t - 13)):
             return t
-    return 16
+    return 19
 
 
 def test_stage12_integers():
@@ -103,12 +106,12 @@ def test_stage12_integers():
     assert g["stats"]["sum_u"] == tot
     want = [_classify(int(x), B.shape[1]) for x in u]
     np.testing.assert_array_equal(g["tier"], np.array(want))
-    counts = np.bincount(np.array(want), minlength=17)
+    counts = np.bincount(np.array(want), minlength=20)
     from paper_1504_05022_b200 import TIER_NAMES
     assert g["stats"]["tier_rows"] == {TIER_NAMES[t]: int(c) for t, c in enumerate(counts) if c}
 
 
-@pytest.mark.parametrize("tier", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("tier", list(range(1, 20)))
 def test_forced_tier(tier):
     """Every row that a class can hold is routed through it; results agree with the oracle
     (and so with every other class: P11 tier-forced agreement)."""
@@ -121,7 +124,7 @@ def test_forced_tier(tier):
     compare(g, R, exact=True, what="tier %d" % tier)
 
 
-@pytest.mark.parametrize("tier", [3, 6, 7, 9, 11, 12, 13, 15, 16])
+@pytest.mark.parametrize("tier", [3, 6, 7, 9, 11, 12, 13, 15, 16, 17, 18, 19])
 def test_forced_tier_precise(tier):
     """PRECISE strategy: symbolic (structure) and numeric (dense / bitmap) classes agree
     with the oracle when rows are forced through each class."""
