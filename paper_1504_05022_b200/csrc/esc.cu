@@ -5,7 +5,7 @@
 //
 //   1. expand: every product (c, a_ij·b_jk, p) with p its position in the row's product order
 //      (j ascending, then k ascending: the order of Algorithm 1 [P:121-135]);
-//   2. counting sort into NB ≈ u/4 buckets by the monotone bucket b(c) = ⌊(c-lo)·NB/W⌋
+//   2. counting sort into NB ≈ u buckets by the monotone bucket b(c) = ⌊(c-lo)·NB/W⌋
 //      (count, exclusive scan, scatter — shared-memory integer atomics only);
 //   3. each bucket (a few entries) sorted by (c, p) with an insertion sort;
 //   4. compress: equal columns fused in p order — the oracle's accumulation order, so values
@@ -108,7 +108,7 @@ __device__ __forceinline__ void esc_products(const Stage3Args& a, int64_t a0, in
 template <int LOG2U, int NT>
 __global__ void __launch_bounds__(NT, 1) k_cta_esc(Stage3Args a) {
   constexpr int UMAX = 1 << LOG2U;
-  constexpr int NBMAX = UMAX / 4;
+  constexpr int NBMAX = UMAX;  // ~1 product per bucket: the per-bucket sorts are trivial
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   const bool fill = a.mode == MODE_FILL;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(NT, 1) k_cta_esc(Stage3Args a) {
       u += s_red[2 * NW + k];
     }
     int NB = 32;
-    while (NB < NBMAX && 4 * NB < u) NB <<= 1;
+    while (NB < NBMAX && NB < u) NB <<= 1;
     const float scale = (float)NB / (float)(int64_t(hi) - lo + 1);
     for (int b = threadIdx.x; b <= NB; b += NT) bstart[b] = 0;
     __syncthreads();
@@ -278,7 +278,7 @@ template <int LOG2U, int NT>
 cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
   constexpr int UMAX = 1 << LOG2U;
   const bool fill = a.mode == MODE_FILL;
-  const size_t sm = size_t(UMAX) * (fill ? 16 : 4) + size_t(UMAX / 4) * 8 + 8;
+  const size_t sm = size_t(UMAX) * (fill ? 16 : 4) + size_t(UMAX) * 8 + 8;
   auto kern = k_cta_esc<LOG2U, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

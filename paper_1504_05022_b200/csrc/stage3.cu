@@ -846,9 +846,16 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
       if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<11, 1, MODE_FILL>, 32, 0, a.count, 1, a, s);
       if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<11, 2, MODE_STRUCT>, 64, 0, a.count, 2, a, s);
       return launch_persistent(k_warp_hash<11, 4, MODE_COUNT>, 128, 0, a.count, 4, a, s);
+    // bucket ESC for values; counting only needs distinct keys: the CTA hash of the same size
     case T_E2048:
+      if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * 4, a.count, 1, a, s);
+      return launch_esc(tier, a, s);
     case T_E4096:
-    case T_E8192: return launch_esc(tier, a, s);
+      if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * 4, a.count, 1, a, s);
+      return launch_esc(tier, a, s);
+    case T_E8192:
+      if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * 4, a.count, 1, a, s);
+      return launch_esc(tier, a, s);
     case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
     case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
     case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);
