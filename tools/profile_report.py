@@ -35,19 +35,33 @@ def raw(rep):
 
 
 def sass_top(rep, n=12):
+    """Per kernel section of the source page: top SASS lines by warp-stall samples."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    if len(rows) < 3:
-        return []
-    h = rows[1]
-    ix = {k: i for i, k in enumerate(h)}
-    data = [r for r in rows[2:] if len(r) > ix.get("Instructions Executed", 0)]
+    sections, cur = [], None
+    for i, r in enumerate(rows):
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1] if len(r) > 1 else "", "hdr": None, "data": []}
+            sections.append(cur)
+        elif cur is not None and cur["hdr"] is None:
+            cur["hdr"] = r
+        elif cur is not None:
+            cur["data"].append(r)
+    res = []
     key = "Warp Stall Sampling (All Samples)"
-    tot = sum(int(r[ix[key]] or 0) for r in data) or 1
-    top = sorted(data, key=lambda r: -int(r[ix[key]] or 0))[:n]
-    return [(100.0 * int(r[ix[key]] or 0) / tot, int(r[ix["Instructions Executed"]] or 0), r[ix["Source"]].strip())
-            for r in top]
+    for sec in sections:
+        h = sec["hdr"] or []
+        if key not in h or "Instructions Executed" not in h:
+            continue
+        ix = {k: i for i, k in enumerate(h)}
+        data = [r for r in sec["data"] if len(r) > ix["Instructions Executed"] and r[ix[key]].isdigit()]
+        tot = sum(int(r[ix[key]]) for r in data) or 1
+        top = sorted(data, key=lambda r: -int(r[ix[key]]))[:n]
+        res.append((sec["name"], [(100.0 * int(r[ix[key]]) / tot, int(r[ix["Instructions Executed"]] or 0),
+                                   r[ix["Source"]].strip()) for r in top],
+                    sum(int(r[ix["Instructions Executed"]] or 0) for r in data)))
+    return res
 
 
 def launches(path):
@@ -88,9 +102,9 @@ def main():
                 if m in h:
                     lines.append("| %s (`%s`) | %s %s |" % (label, m, v[h.index(m)], units[h.index(m)]))
             lines.append("")
-        top = sass_top(rep)
-        if top:
-            lines.append("Top SASS lines by warp-stall samples (share of samples, executions):\n")
+        for kname, top, ninstr in sass_top(rep):
+            lines.append("Top SASS lines of `%s` by warp-stall samples (share of samples, warp-level "
+                         "executions); %d warp instructions in total:\n" % (kname, ninstr))
             lines.append("```")
             for pct, ex, src in top:
                 lines.append("%5.1f%% %12d  %s" % (pct, ex, src))
