@@ -320,20 +320,33 @@ __device__ __forceinline__ unsigned warp_insert(int* keys, int c, bool act, int&
   constexpr unsigned MASK = (1u << LOG2S) - 1;
   unsigned h = hslot<LOG2S>(c);
   int k = keys[h];
-  bool pend = act && k != c;
+  // fast path, straight-line: a new key claims its empty home slot with one CAS
+  const int claim = act && k == kEmptyKey;
+  int pend = act && k != c;
+  if (__any_sync(0xffffffffu, claim)) {
+    if (claim) {
+      const int old = atomicCAS(&keys[h], kEmptyKey, c);
+      if (old == kEmptyKey || old == c) {
+        inserted += old == kEmptyKey;
+        pend = 0;
+      } else {
+        k = old;  // lost to another column of this instruction: probe on
+      }
+    }
+  }
+  // slow path: home slot held by another column (probe linearly)
   while (__any_sync(0xffffffffu, pend)) {
     if (pend) {
-      if (k == kEmptyKey) {
+      if (k == c) {
+        pend = 0;
+      } else if (k == kEmptyKey) {
         const int old = atomicCAS(&keys[h], kEmptyKey, c);
         if (old == kEmptyKey || old == c) {
           inserted += old == kEmptyKey;
-          pend = false;
+          pend = 0;
         } else {
-          h = (h + 1) & MASK;
-          k = keys[h];
+          k = old;
         }
-      } else if (k == c) {
-        pend = false;
       } else {
         h = (h + 1) & MASK;
         k = *(volatile int*)&keys[h];
