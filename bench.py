@@ -45,17 +45,32 @@ BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
 
 # ----------------------------------------------------------------------------- inputs
+def _device_gen():
+    """Torch generators on the GPU when one is present (bit-identical to gen/'s numpy)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from gen import torchgen
+            return torchgen
+    except Exception:
+        pass
+    return None
+
+
 def make_workload(cfg: str, scale: int | None = None):
-    """Returns a list of (name, A, B) products; B None means B = A."""
+    """Returns a list of (name, A, B) products; B None means B = A, "prev" = previous output."""
     import gen
+    tg = _device_gen()
     if cfg == "c1":
         return [("A2", gen.stencil("2d5", 32), None)]
     if cfg == "c2":
         return [("A2", gen.stencil("3d27", scale or 128), None)]
-    if cfg == "c3a":
-        return [("A2", gen.rmat(scale or 22, 16, (0.45, 0.15, 0.15, 0.25), seed=gen.SEED, mode="real"), None)]
-    if cfg == "c3b":
-        return [("A2", gen.rmat(scale or 18, 16, (0.57, 0.19, 0.19, 0.05), seed=gen.SEED, mode="real"), None)]
+    if cfg in ("c3a", "c3b"):
+        sc = scale or (22 if cfg == "c3a" else 18)
+        abcd = (0.45, 0.15, 0.15, 0.25) if cfg == "c3a" else (0.57, 0.19, 0.19, 0.05)
+        if tg is not None:
+            return [("A2", tg.to_csr(*tg.rmat(sc, 16, abcd, seed=gen.SEED, mode="real")), None)]
+        return [("A2", gen.rmat(sc, 16, abcd, seed=gen.SEED, mode="real"), None)]
     if cfg in ("c4a", "c4b"):
         n = scale or 256
         A = gen.stencil("3d7", n)
@@ -64,6 +79,8 @@ def make_workload(cfg: str, scale: int | None = None):
         return [("AP", A, P), ("R(AP)", R, "prev")]
     if cfg == "c5":
         n = 1 << (scale or 23)
+        if tg is not None:
+            return [("AB", tg.to_csr(*tg.band(n)), tg.to_csr(*tg.uniform_rows(n, n, 64)))]
         return [("AB", gen.band(n), gen.uniform_rows(n, n, 64))]
     raise SystemExit("unknown config %s" % cfg)
 
@@ -163,19 +180,55 @@ def run_gpu(args):
 
     dist_ops = {}
 
+    # Row blocks per product.  c5's C (412 GB at n = 2^23) cannot be resident: each rank runs
+    # its rows in waves (C of a wave is freed before the next); the per-rank nnz are still
+    # all-gathered for the global row offsets.  Other configs: one block (dist_* for N > 1).
+    def plan_blocks(A, Bm):
+        m = A.shape[0]
+        if args.config != "c5" or Bm is None or isinstance(Bm, str):
+            return [(0, m)]
+        r0, r1 = (rank * m) // world, ((rank + 1) * m) // world
+        bl = np.diff(Bm.rp)
+        u_rows = np.zeros(m, dtype=np.int64)
+        np.add.at(u_rows, np.repeat(np.arange(m), np.diff(A.rp)), bl[A.ci])
+        est = 16 * int(u_rows[r0:r1].sum())  # C (12 B) + structure set (4 B) per product
+        budget = int(args.wave_gb * (1 << 30))
+        waves = max(1, -(-est // budget))
+        cuts = [r0 + ((r1 - r0) * w) // waves for w in range(waves + 1)]
+        return list(zip(cuts[:-1], cuts[1:]))
+
+    blocks_of = {}
+    for (name, A, B, dA, dB) in dev_inputs:
+        blocks_of[name] = plan_blocks(A, A if B is None else B)
+    sharded = args.config == "c5"
+
     def one_step(collect=False):
         """Whole hot path once: every product of the workload, symbolic + numeric."""
         out = None
         info = []
         for (name, A, B, dA, dB) in dev_inputs:
             Bm = dA if dB is None else (out if isinstance(dB, str) else dB)
-            if world == 1:
-                op = sg.SpGEMM(dA, Bm, flags, stream)
-                nnz = op.symbolic()
-                out = op.numeric()
-                if collect:
-                    info.append((name, op.stats(), nnz, dA, Bm))
-                op.destroy()
+            if world == 1 or sharded:
+                blocks = blocks_of[name]
+                tot_nnz = 0
+                for (r0, r1) in blocks:
+                    dAb = dA if (r0, r1) == (0, dA.rows) else sg.DeviceCsr(r1 - r0, dA.cols, dA.rp[r0:r1 + 1],
+                                                                          dA.ci, dA.val)
+                    op = sg.SpGEMM(dAb, Bm, flags, stream)
+                    nnz = op.symbolic()
+                    out = op.numeric()
+                    tot_nnz += nnz
+                    if collect:
+                        info.append((name, op.stats(), nnz, dAb, Bm))
+                    op.destroy()
+                    if len(blocks) > 1:
+                        out = None  # capacity-forced waves: the wave's C is released
+                if sharded and world > 1:
+                    # stitching: every rank learns the nnz of all row blocks (global offsets)
+                    t = torch.tensor([tot_nnz], dtype=torch.int64, device="cuda")
+                    allt = [torch.empty_like(t) for _ in range(world)]
+                    with torch.cuda.stream(stream):
+                        dist.all_gather(allt, t)
             else:
                 # the NCCL communicator is created once (outside the timed steps); each step
                 # re-runs the partition, the local four stages and the nnz allgather
@@ -247,11 +300,22 @@ def run_gpu(args):
     cb = 0
     nnz_c_tot = 0
     launches = 0
+    seen_b = set()
     for name, st, nnz_c, dA, Bm in info:
         m = dA.rows
-        cb += csr_bytes(m, dA.nnz) + csr_bytes(Bm.rows, Bm.nnz) + csr_bytes(m, nnz_c)
+        a_nnz = int(dA.rp[-1].item() - dA.rp[0].item()) if m > 0 else 0  # a row block's own entries
+        cb += csr_bytes(m, a_nnz) + csr_bytes(m, nnz_c)
+        if (name, id(Bm)) not in seen_b:  # B is read once per product even across waves
+            cb += csr_bytes(Bm.rows, Bm.nnz)
+            seen_b.add((name, id(Bm)))
         nnz_c_tot += nnz_c
         launches += st["launches_symbolic"] + st["launches_numeric"]
+    if sharded and world > 1:
+        t = torch.tensor([nnz_c_tot, cb - sum(csr_bytes(d[4].rows, d[4].nnz) for d in info[:1])],
+                         dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        nnz_c_tot = int(t[0].item())
+        cb = int(t[1].item()) + csr_bytes(info[0][4].rows, info[0][4].nnz)
     gflops = 2.0 * sum_u / (ms_step * 1e-3) / 1e9
     peaks = {}
     try:
@@ -301,7 +365,7 @@ def run_gpu(args):
 
     # ---------------- end-to-end through the public API with host buffers ----------------
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and all(len(b) == 1 for b in blocks_of.values()):
         e2e = e2e_measure(args, work, flags, stream, sum_u)
 
     result = {
@@ -323,6 +387,7 @@ def run_gpu(args):
                    "nnz_a": int(sum(d[3].nnz for d in dev_inputs)),
                    "parallelism": "row blocks x%d (dist_* ABI, NCCL)" % world if world > 1 else "1 GPU",
                    "l2": "flushed before every timed step (512 MiB memset, outside the timed window)",
+                   "waves": {n: len(b) for n, b in blocks_of.items() if len(b) > 1} or None,
                    "scale": args.scale},
         "hbm": {"compulsory_bytes": cb, "achieved_gbs": round(step_gbs, 1),
                 "frac_of_peak": round(step_gbs / hbm_peak, 4), "peak_gbs": hbm_peak,
@@ -525,6 +590,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--wave-gb", type=float, default=80.0, help="c5: device memory budget per row wave")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
