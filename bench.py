@@ -339,7 +339,7 @@ def run_gpu(args):
         if not hybrid:
             sym_ms = st0["stage_ms"][1]
             alg = 28 * m0 + 4 * dA0.nnz + 4 * min(Bm0.nnz, st0["sum_u"]) + 4 * nnz0
-            cands.append((sym_ms, alg, "%s: symbolic stage-3 structure pass (k_warp_hash STRUCT / counts)" % name0,
+            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bwrow COUNT / k_wrow STRUCT / counts)" % name0,
                           "symbolic"))
         for cls_name, c in st0["classes"].items():
             if c["ms"] <= 0:
@@ -347,7 +347,8 @@ def run_gpu(args):
             dense = (not hybrid) and cls_name.startswith("w")
             alg = (36 if dense else 28) * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + \
                 12 * c["c_entries"] + (4 * c["c_entries"] if dense else 0)
-            kname = ("k_warp_dense" if dense else "k_warp_hash") if cls_name.startswith("w") else \
+            kname = "k_bwrow" if cls_name == "bw" else \
+                ("k_wdense" if dense else "k_wrow") if cls_name.startswith("w") else \
                 "k_group" if cls_name.startswith("g") else "k_cta_esc" if cls_name.startswith("e") else \
                 "k_cta_hash" if cls_name.startswith("c") else ("k_long" if hybrid else "k_long_bm_fill")
             cands.append((c["ms"], alg, "%s: stage-3 class %s (%s)" % (name0, cls_name, kname), cls_name))

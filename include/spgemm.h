@@ -67,7 +67,7 @@ enum {
 };
 
 /* Number of stage-2 size classes ("bins", re-derived for 228 KB smem/SM). */
-#define SPGEMM_NUM_TIERS 20
+#define SPGEMM_NUM_TIERS 21
 
 typedef struct spgemm_stats {
   int64_t m, k, n, nnz_a, nnz_b;

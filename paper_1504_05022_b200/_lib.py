@@ -10,10 +10,10 @@ import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libspgemm.so")
-NUM_TIERS = 20
+NUM_TIERS = 21
 
 TIER_NAMES = ["empty", "g1", "g2", "g4", "g8", "g16", "g32", "w64", "w128", "w256", "w512", "w1024",
-              "w2048", "c2048", "c4096", "c8192", "e2048", "e4096", "e8192", "long"]
+              "w2048", "c2048", "c4096", "c8192", "e2048", "e4096", "e8192", "bw", "long"]
 
 STATUS = {
     0: "SPGEMM_SUCCESS", 1: "SPGEMM_ERROR_INVALID_VALUE", 2: "SPGEMM_ERROR_INVALID_CSR",

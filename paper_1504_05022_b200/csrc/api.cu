@@ -124,6 +124,7 @@ struct spgemm_handle_s {
   int64_t tier_count[NUM_TIERS] = {};
   int64_t tier_off[NUM_TIERS + 1] = {};
   int64_t sum_u = 0, max_u = 0, sum_cap = 0;
+  int64_t bw_wmax = 0, bw_vmax = 0;  // T_BW class: largest window, row length
   bool sym_ok = false;
   int64_t nnz_c = 0;
   std::string err;
@@ -510,6 +511,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   AL(h, &ws.blk_usum, ws.nblk);
   AL(h, &ws.blk_umax, ws.nblk);
   AL(h, &ws.summary, kSumLen);
+  AL(h, &ws.bwin, h->k > 0 ? h->k : 1);
+  AL(h, &ws.rlo, m);
   AL(h, &h->nnz_row, m);
   AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
   // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
@@ -519,7 +522,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = false;
   // C~ offsets in both strategies: hybrid keeps whole rows there, precise only the sorted
   // column sets of the warp classes (4 B/entry) for its numeric pass
-  CK(h, launch_stage1(m, h->n, h->A, h->B.rp, tp, true, ws, h->stream));
+  CK(h, launch_stage1(m, h->k, h->n, h->A, h->B, tp, true, ws, h->stream));
   CK(h, launch_stage2(m, ws, true, h->n, h->stream));
   h->launches_sym = 3;
   tr("alloc + stage 1-2");
@@ -535,7 +538,15 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->sum_u = h->pinned[kSumU];
   h->sum_cap = h->pinned[kSumCap];
   h->max_u = h->pinned[kSumUMax];
-  AL(h, &h->ctil_col, h->sum_cap);
+  h->bw_wmax = h->pinned[kSumWmax];
+  h->bw_vmax = h->pinned[kSumVmax];
+  {
+    // precise: C~ holds only the warp classes' sorted column sets (STRUCT)
+    bool need = hybrid;
+    for (int t = T_W64; t <= T_W2048; ++t) need = need || h->tier_count[t] > 0;
+    need = need || h->tier_count[T_BW] > 0;
+    AL(h, &h->ctil_col, need ? h->sum_cap : 1);
+  }
   if (hybrid) AL(h, &h->ctil_val, h->sum_cap);
   tr("C~ allocation");
   cudaEventRecord(h->ev[1], h->stream);
@@ -545,6 +556,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     Stage3Args a{};
     a.A = h->A;
     a.B = h->B;
+    a.b_nnz = h->b_nnz;
     a.n = h->n;
     a.perm = ws.perm;
     a.first = h->tier_off[t];
@@ -553,7 +565,10 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.out_col = h->ctil_col;
     a.out_val = h->ctil_val;
     a.nnz_row = h->nnz_row;
-    a.mode = hybrid ? MODE_FILL : (t >= T_W64 && t <= T_W2048) ? MODE_STRUCT : MODE_COUNT;
+    a.mode = hybrid ? MODE_FILL : ((t >= T_W64 && t <= T_W2048) || t == T_BW) ? MODE_STRUCT : MODE_COUNT;
+    a.rlo = ws.rlo;
+    a.bw_wmax = h->bw_wmax;
+    a.bw_vmax = h->bw_vmax;
     cudaEventRecord(h->tev[t][0], h->stream);
     CK(h, launch_stage3_tier(t, a, h->stream));
     cudaEventRecord(h->tev[t][1], h->stream);
@@ -574,6 +589,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     Stage3Args a{};
     a.A = h->A;
     a.B = h->B;
+    a.b_nnz = h->b_nnz;
     a.n = h->n;
     a.perm = ws.perm;
     a.first = h->long_first;
@@ -612,6 +628,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->tier_off[NUM_TIERS] = h->pinned[kSumOff + NUM_TIERS];
     h->nlong = h->tier_count[T_LONG];
     h->long_first = h->tier_off[T_LONG];
+    h->bw_vmax = h->pinned[kSumVmax];  // exact: max nnz(c_i*) over the window rows
     tr("re-binning");
   }
   h->sym_ok = true;
@@ -652,6 +669,8 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         Stage3Args a{};
         a.A = h->A;
         a.B = h->B;
+        a.b_nnz = h->b_nnz;
+    a.b_nnz = h->b_nnz;
         a.n = h->n;
         a.perm = h->ws.perm;
         a.first = h->tier_off[t];
@@ -660,10 +679,13 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.out_col = c_col_idx;
         a.out_val = c_val;
         a.nnz_row = nullptr;
-        const bool dense = t >= T_W64 && t <= T_W2048;
+        const bool dense = (t >= T_W64 && t <= T_W2048) || t == T_BW;
         a.mode = dense ? MODE_DENSE : MODE_FILL;
         a.struct_col = h->ctil_col;
         a.struct_off = h->ws.ctil_off;
+        a.rlo = h->ws.rlo;
+        a.bw_wmax = h->bw_wmax;
+        a.bw_vmax = h->bw_vmax;
         cudaEventRecord(h->tev[t][0], h->stream);
         CK(h, launch_stage3_tier(t, a, h->stream));
         cudaEventRecord(h->tev[t][1], h->stream);
@@ -674,6 +696,8 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         Stage3Args a{};
         a.A = h->A;
         a.B = h->B;
+        a.b_nnz = h->b_nnz;
+    a.b_nnz = h->b_nnz;
         a.n = h->n;
         a.perm = h->ws.perm;
         a.first = h->long_first;

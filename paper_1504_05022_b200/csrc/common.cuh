@@ -14,6 +14,10 @@
 //   T_E2048..T_E8192   u <= U (cap > 1638)        one CTA per row, bucket ESC: products counting-
 //                                                 sorted into buckets (monotone bucket function),
 //                                                 each bucket sorted by (column, product index)
+//   T_BW               u > 32, W <= 2^17,         one warp per row, dense bitmap over the row's
+//                      min(u,W) <= 2048           column window [lo, lo+W) (the SPA of [P:142]
+//                                                 restricted to the window), 2-level for sparse
+//                                                 windows; W = max_j max(b_j*) - min_j min(b_j*) + 1
 //   T_LONG             otherwise                  progressive global table + re-allocation
 //                                                 (group 5, [P:286-297])
 #pragma once
@@ -30,20 +34,30 @@ enum Tier : int {
   T_W64 = 7, T_W128 = 8, T_W256 = 9, T_W512 = 10, T_W1024 = 11, T_W2048 = 12,
   T_C2048 = 13, T_C4096 = 14, T_C8192 = 15,
   T_E2048 = 16, T_E4096 = 17, T_E8192 = 18,
-  T_LONG = 19,
-  NUM_TIERS = 20
+  T_BW = 19,
+  T_LONG = 20,
+  NUM_TIERS = 21
 };
 static_assert(NUM_TIERS == SPGEMM_NUM_TIERS, "tier count mismatch with the ABI header");
 
 constexpr int kEmptyKey = -1;
+
+// Window-bitmap class limits: column window W (bits per warp) and row length (values per warp).
+constexpr int64_t kBwMaxW = int64_t(1) << 17;
+constexpr int64_t kBwMaxV = 2048;
+
+__host__ __device__ inline bool bw_ok(int64_t cap, int64_t W) {
+  return W > 0 && W <= kBwMaxW && (cap < W ? cap : W) <= kBwMaxV;
+}
 
 struct TierParams {
   int force_tier;         // -1 = off
   int64_t long_threshold; // rows with cap above go long (0 = default by smem)
 };
 
-__host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap) {
+__host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap, int64_t W) {
   if (t == T_EMPTY) return u == 0;
+  if (t == T_BW) return bw_ok(cap, W);
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
   if (t >= T_W64 && t <= T_W2048) {
     int64_t S = int64_t(64) << (t - T_W64);
@@ -61,22 +75,24 @@ __host__ __device__ inline int esc_class(int64_t u) {
 }
 
 // Stage-2 classification of one row (the B200 re-derivation of Algorithm 3 [P:226-260]).
-__host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
+// W: the row's column window (0 when u = 0).
+__host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p, int64_t W) {
   if (u == 0) return T_EMPTY;
   int64_t cap = u < n ? u : n;
-  if (p.force_tier >= 0 && u >= 2 && tier_capacity_ok(p.force_tier, u, cap)) return p.force_tier;
+  if (p.force_tier >= 0 && u >= 2 && tier_capacity_ok(p.force_tier, u, cap, W)) return p.force_tier;
   if (p.long_threshold > 0 && cap > p.long_threshold) return T_LONG;
   if (u <= 32) {
     int g = 0;
     while ((int64_t(1) << g) < u) ++g;
     return T_G1 + g;
   }
+  if (bw_ok(cap, W)) return T_BW;
   for (int t = T_W64; t <= T_W2048; ++t)
-    if (tier_capacity_ok(t, u, cap)) return t;
+    if (tier_capacity_ok(t, u, cap, W)) return t;
   const int e = esc_class(u);  // products fit one CTA's shared memory: bucket ESC
   if (e >= 0) return e;
   for (int t = T_C2048; t <= T_C8192; ++t)
-    if (tier_capacity_ok(t, u, cap)) return t;
+    if (tier_capacity_ok(t, u, cap, W)) return t;
   return T_LONG;
 }
 
@@ -84,6 +100,7 @@ __host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p) {
 // by it (load <= 1/2) instead of by the bound min(u_i, n).
 __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
   if (t == T_EMPTY) return u == 0;
+  if (t == T_BW) return 0;  // only rows that were window rows in the symbolic pass (below)
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
   if (t >= T_W64 && t <= T_W2048) return (int64_t(64) << (t - T_W64)) >= 2 * nnz;  // dense: S >= 2·nnz
   if (t >= T_C2048 && t <= T_C8192) return nnz <= (int64_t(2048) << (t - T_C2048));
@@ -95,6 +112,7 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
 // that only the symbolic warp classes (STRUCT) produce.
 __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_class, TierParams p) {
   if (u == 0) return T_EMPTY;
+  if (sym_class == T_BW) return T_BW;  // window and bound unchanged: nnz <= min(u, W) <= kBwMaxV
   const bool has_struct = sym_class >= T_W64 && sym_class <= T_W2048;
   if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz) &&
       (has_struct || p.force_tier < T_W64 || p.force_tier > T_W2048) &&
@@ -138,6 +156,7 @@ enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1, MODE_STRUCT = 2, MODE_DENSE = 3
 struct Stage3Args {
   CsrView A, B;
   int64_t n;
+  int64_t b_nnz;         // nnz(B): 32-bit entry offsets below 2^31
   const int32_t* perm;   // rows grouped by tier
   int64_t first;         // this tier's rows are perm[first, first + count)
   int64_t count;
@@ -148,6 +167,8 @@ struct Stage3Args {
   int mode;
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
+  const int32_t* rlo;         // T_BW: first column of each row's window
+  int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
 };
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------
@@ -160,7 +181,9 @@ struct Stage12Ws {
   int64_t* blk_cap;    // [nblk]
   int64_t* blk_usum;   // [nblk]
   int64_t* blk_umax;   // [nblk]
-  int64_t* summary;    // [NUM_TIERS (counts) + NUM_TIERS+1 (offsets) + 3] device
+  int64_t* summary;    // [kSumLen] device
+  int2* bwin;          // [k] (min, max) column of each row of B; (INT_MAX, -1) if empty
+  int32_t* rlo;        // [m] first column of each row's window
   int64_t nblk;
 };
 constexpr int kS12Threads = 256;
@@ -172,9 +195,12 @@ constexpr int kSumOff = NUM_TIERS;                 // tier offsets [NUM_TIERS+1]
 constexpr int kSumU = 2 * NUM_TIERS + 1;           // sum u
 constexpr int kSumCap = kSumU + 1;                 // sum cap (C~ entries)
 constexpr int kSumUMax = kSumU + 2;                // max u
-constexpr int kSumLen = kSumU + 3;
+constexpr int kSumWmax = kSumU + 3;              // max W over T_BW rows
+constexpr int kSumVmax = kSumU + 4;              // max min(u, W) over T_BW rows (after re-binning:
+                                                 // max nnz(c_i*))
+constexpr int kSumLen = kSumU + 5;
 
-cudaError_t launch_stage1(int64_t m, int64_t n, CsrView A, const int64_t* b_rp, TierParams tp,
+cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           bool hybrid_caps, Stage12Ws& ws, cudaStream_t s);
 cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n, cudaStream_t s);
 // PRECISE: re-bin rows by (u_i, nnz(c_i*)) into ws.tier/perm (ws.U and nnz_row are inputs).
@@ -182,6 +208,11 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
                          cudaStream_t s);
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
+// warp classes T_W64..T_W2048 (warp.cu)
+cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s);
+// window-bitmap class T_BW (warp.cu)
+cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s);
+int num_sms();
 // bucket-ESC classes (esc.cu)
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s);
 // PRECISE long rows: bitmap over the column window (COUNT: nnz; FILL: ranks → C)

@@ -8,6 +8,8 @@
 //   k_stage2_scan     one CTA: class offsets (class-major, block order) + capacity offsets
 //   k_stage2_scatter  stable scatter of row ids into perm (ascending row id within a
 //                     class: deterministic) + exclusive scan of capacities → C~ offsets
+#include <climits>
+
 #include <cub/warp/warp_reduce.cuh>
 
 #include "common.cuh"
@@ -53,46 +55,84 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* total, in
 }
 
 // ---------------------------------------------------------------------------- stage 1
-// Algorithm "first stage" [P:198-212]: one thread per entry of U, u_i = sum nnz(b_j*).
+// Per row j of B: its first and last column, (INT_MAX, -1) when empty (rows are sorted, Q3).
+__global__ void k_bwin(int64_t k, const int64_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                       int2* __restrict__ bwin) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const int64_t b0 = __ldg(brp + j), b1 = __ldg(brp + j + 1);
+  bwin[j] = b1 > b0 ? make_int2(__ldg(bci + b0), __ldg(bci + b1 - 1)) : make_int2(INT_MAX, -1);
+}
+
+__device__ __forceinline__ void acc_row(int64_t& u, int& lo, int& hi, const int64_t* brp, const int2* bwin,
+                                        int j) {
+  u += __ldg(brp + j + 1) - __ldg(brp + j);  // line 4: u_i += nnz(b_j*)
+  const int2 w = __ldg(bwin + j);
+  lo = min(lo, w.x);
+  hi = max(hi, w.y);
+}
+
+// Algorithm "first stage" [P:198-212]: one thread per entry of U, u_i = sum nnz(b_j*); with it
+// the row's column window [lo, hi] (for the window-bitmap class) and the class of the row.
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
-                                               const int64_t* __restrict__ brp, TierParams tp,
+                                               const int64_t* __restrict__ brp,
+                                               const int2* __restrict__ bwin, TierParams tp,
                                                int hybrid, int64_t* __restrict__ U,
-                                               uint8_t* __restrict__ tier,
+                                               uint8_t* __restrict__ tier, int32_t* __restrict__ rlo,
                                                int32_t* __restrict__ blk_tier,
                                                int64_t* __restrict__ blk_cap,
                                                int64_t* __restrict__ blk_usum,
-                                               int64_t* __restrict__ blk_umax) {
+                                               int64_t* __restrict__ blk_umax,
+                                               int64_t* __restrict__ summary) {
   __shared__ int s_hist[NUM_TIERS];
   __shared__ int64_t s_red[3][NT / 32];
   if (threadIdx.x < NUM_TIERS) s_hist[threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * NT * RPT;
-  int64_t capsum = 0, usum = 0, umax = 0;
+  int64_t capsum = 0, usum = 0, umax = 0, wmax = 0, vmax = 0;
 #pragma unroll 1
   for (int r = 0; r < RPT; ++r) {
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     if (i < m) {
       const int64_t a0 = __ldg(A.rp + i), a1 = __ldg(A.rp + i + 1);
       int64_t u = 0;                                     // line 2: u_i <- 0
+      int lo = INT_MAX, hi = -1;
       int64_t p = a0;
       for (; p + 4 <= a1; p += 4) {                      // line 3: each a_ij in a_i*
         const int j0 = __ldg(A.ci + p), j1 = __ldg(A.ci + p + 1);
         const int j2 = __ldg(A.ci + p + 2), j3 = __ldg(A.ci + p + 3);
-        u += (__ldg(brp + j0 + 1) - __ldg(brp + j0)) + (__ldg(brp + j1 + 1) - __ldg(brp + j1)) +
-             (__ldg(brp + j2 + 1) - __ldg(brp + j2)) + (__ldg(brp + j3 + 1) - __ldg(brp + j3));
+        acc_row(u, lo, hi, brp, bwin, j0);
+        acc_row(u, lo, hi, brp, bwin, j1);
+        acc_row(u, lo, hi, brp, bwin, j2);
+        acc_row(u, lo, hi, brp, bwin, j3);
       }
-      for (; p < a1; ++p) {
-        const int j = __ldg(A.ci + p);
-        u += __ldg(brp + j + 1) - __ldg(brp + j);        // line 4: u_i += nnz(b_j*)
-      }
-      const int t = classify(u, n, tp);
+      for (; p < a1; ++p) acc_row(u, lo, hi, brp, bwin, __ldg(A.ci + p));
+      const int64_t W = hi >= lo ? int64_t(hi) - lo + 1 : 0;
+      const int t = classify(u, n, tp, W);
       U[i] = u;
       tier[i] = (uint8_t)t;
+      rlo[i] = lo;
       atomicAdd(&s_hist[t], 1);
       capsum += hybrid ? hybrid_capacity(t, u, n) : 0;
       usum += u;
       umax = u > umax ? u : umax;
+      if (t == T_BW) {
+        wmax = W > wmax ? W : wmax;
+        const int64_t v = u < W ? u : W;
+        vmax = v > vmax ? v : vmax;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, wmax > 0)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      wmax = max(wmax, (int64_t)__shfl_xor_sync(0xffffffffu, wmax, o));
+      vmax = max(vmax, (int64_t)__shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumWmax), (unsigned long long)wmax);
+      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), (unsigned long long)vmax);
     }
   }
   // block reductions
@@ -130,7 +170,7 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
                                               const int64_t* __restrict__ nnz_row, TierParams tp,
                                               uint8_t* __restrict__ tier, int32_t* __restrict__ blk_tier,
                                               int64_t* __restrict__ blk_cap, int64_t* __restrict__ blk_usum,
-                                              int64_t* __restrict__ blk_umax) {
+                                              int64_t* __restrict__ blk_umax, int64_t* __restrict__ summary) {
   __shared__ int s_hist[NUM_TIERS];
   if (threadIdx.x < NUM_TIERS) s_hist[threadIdx.x] = 0;
   __syncthreads();
@@ -141,6 +181,8 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
       const int t = classify_exact(U[i], nnz_row[i], (int)tier[i], tp);
       tier[i] = (uint8_t)t;
       atomicAdd(&s_hist[t], 1);
+      if (t == T_BW)
+        atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), (unsigned long long)nnz_row[i]);
     }
   }
   __syncthreads();
@@ -359,12 +401,15 @@ __global__ void k_validate(int64_t rows, int64_t cols, const int64_t* __restrict
 
 }  // namespace
 
-cudaError_t launch_stage1(int64_t m, int64_t n, CsrView A, const int64_t* b_rp, TierParams tp,
+cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           bool hybrid_caps, Stage12Ws& ws, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 2 * sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
+  if (k > 0) k_bwin<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, B.rp, B.ci, ws.bwin);
   k_stage1<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, A, b_rp, tp, hybrid_caps ? 1 : 0, ws.U, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum,
-      ws.blk_umax);
+      m, n, A, B.rp, ws.bwin, tp, hybrid_caps ? 1 : 0, ws.U, ws.tier, ws.rlo, ws.blk_tier, ws.blk_cap,
+      ws.blk_usum, ws.blk_umax, ws.summary);
   return cudaGetLastError();
 }
 
@@ -381,9 +426,11 @@ cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n,
 cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParams tp, Stage12Ws& ws,
                          cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(ws.summary + kSumVmax, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
   k_rebin<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, ws.U, nnz_row, tp, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax);
-  cudaError_t e = cudaGetLastError();
+      m, n, ws.U, nnz_row, tp, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax, ws.summary);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_stage2(m, ws, false, n, s);
 }

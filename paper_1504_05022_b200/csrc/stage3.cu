@@ -9,15 +9,12 @@
 //   k_group<G>   u_i <= G <= 32: G lanes per row, lane = one product; the products are
 //                sorted by (column, product index) with a register bitonic network and
 //                fused left to right — the ESC idea with the whole row in registers.
-//   k_warp_hash  one warp per row, S-slot shared-memory hash; lanes walk one row b_j* at a
-//                time (columns within a row of B are distinct, so no two lanes of one
-//                instruction touch one slot); accumulation order per column = j ascending.
-//                Then compaction + shared-memory bitonic sort (the paper's ESC sort step).
+//   (warp.cu)    one warp per row, S-slot shared-memory hash (classes w64..w2048).
 //   k_cta_hash   one CTA per row, order-preserving hash (home slot monotone in the column)
 //                with linear probing into 2H slots: clusters come out ordered, only each
 //                cluster is insertion-sorted before the ordered compaction.
 // Values: products are rounded separately (__dmul_rn, no FMA) and summed with __dadd_rn.
-// k_group and k_warp_hash add in j-ascending order starting from the first product (the
+// k_group and the warp classes add in j-ascending order starting from the first product (the
 // warp hash starts from -0.0, the identity of +), i.e. the oracle's order [P:129-131].
 #include <climits>
 
@@ -163,390 +160,6 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
       }
       __syncwarp();
     }
-  }
-}
-
-// --------------------------------------------------------------- warp classes
-// Register bitonic sort of N = 32·E int keys held in "blocked" layout (lane l holds
-// elements l·E .. l·E+E-1): strides < E are in-register, strides >= E cross lanes.
-template <int E>
-__device__ __forceinline__ void warp_bitonic_keys(int (&k)[E], int lane) {
-  constexpr int N = 32 * E;
-#pragma unroll
-  for (int kk = 2; kk <= N; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= E) {
-        const int lj = j / E;
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const int i = lane * E + r;
-          const int p = __shfl_xor_sync(0xffffffffu, k[r], lj);
-          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
-          k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          if (r & j) continue;
-          const int i = lane * E + r;
-          const bool asc = (i & kk) == 0;
-          const int x = k[r], y = k[r | j];
-          k[r] = asc ? min(x, y) : max(x, y);
-          k[r | j] = asc ? max(x, y) : min(x, y);
-        }
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ int ht_find(const int* keys, int c, unsigned mask, int shift) {
-  unsigned h = ((unsigned)c * 0x9E3779B1u) >> shift;
-  while (keys[h] != c) h = (h + 1) & mask;
-  return (int)h;
-}
-
-// Sorted output of a warp table: the keys were compacted into `scratch`; sort them
-// (registers for N <= 128, shared memory above); with VALS fetch each key's value from the
-// intact table.
-template <int E, bool VALS>
-__device__ __forceinline__ void warp_emit_sorted_reg(const int* keys, const double* vals, const int* scratch,
-                                                     int cnt, unsigned mask, int shift, int lane,
-                                                     int32_t* out_col, double* out_val) {
-  int k[E];
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = lane * E + r;
-    k[r] = i < cnt ? scratch[i] : INT_MAX;
-  }
-  warp_bitonic_keys<E>(k, lane);
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = lane * E + r;
-    if (i < cnt) {
-      out_col[i] = k[r];
-      if (VALS) out_val[i] = vals[ht_find(keys, k[r], mask, shift)];
-    }
-  }
-}
-
-template <bool VALS>
-__device__ __forceinline__ void warp_emit_sorted(const int* keys, const double* vals, int* scratch, int cnt,
-                                                 unsigned mask, int shift, int lane, int32_t* oc, double* ov) {
-  if (cnt <= 32) {
-    warp_emit_sorted_reg<1, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
-  } else if (cnt <= 64) {
-    warp_emit_sorted_reg<2, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
-  } else if (cnt <= 128) {
-    warp_emit_sorted_reg<4, VALS>(keys, vals, scratch, cnt, mask, shift, lane, oc, ov);
-  } else {
-    // larger rows: bitonic sort of the scratch keys in shared memory (ESC sort [P:277-284])
-    int N = 1;
-    while (N < cnt) N <<= 1;
-    for (int s = cnt + lane; s < N; s += 32) scratch[s] = INT_MAX;
-    __syncwarp();
-    for (int kk = 2; kk <= N; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < (N >> 1); i += 32) {
-          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-          const int hi = lo + j;
-          const bool asc = (lo & kk) == 0;
-          const int kl = scratch[lo], kh = scratch[hi];
-          if ((kl > kh) == asc) {
-            scratch[lo] = kh;
-            scratch[hi] = kl;
-          }
-        }
-        __syncwarp();
-      }
-    }
-    for (int t = lane; t < cnt; t += 32) {
-      const int kk = scratch[t];
-      oc[t] = kk;
-      if (VALS) ov[t] = vals[ht_find(keys, kk, mask, shift)];
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------------------
-// Warp classes.  One warp per row; lanes walk one b_j* at a time (columns within a row of B
-// are distinct, so no two lanes of one instruction touch one slot).  The next two b_j* are
-// in flight while one is processed (prefetch distance 2).  Tables are static shared arrays
-// so every access is a direct 32-bit shared address.
-//   MODE_COUNT  : insert keys, count                       (precise symbolic, non-warp rows)
-//   MODE_STRUCT : insert keys, count, emit the sorted set  (precise symbolic)
-//   MODE_FILL   : insert keys + accumulate values, emit the sorted row   (hybrid)
-template <int NW>
-struct WarpMeta {
-  const int32_t* pc[NW][32];
-  const double* pv[NW][32];
-  int len[NW][32];
-  double av[NW][32];
-};
-
-// stage up to 32 a_ij of the row: pointers to b_j* and lengths
-template <int NW, bool VALS>
-__device__ __forceinline__ int stage_a_chunk(const Stage3Args& a, WarpMeta<NW>& m, int w, int lane,
-                                             int64_t e0, int64_t a1) {
-  const int64_t e = e0 + lane;
-  const int32_t* pc = a.B.ci;
-  const double* pv = a.B.val;
-  int len = 0;
-  double av = 0.0;
-  if (e < a1) {
-    const int j = __ldg(a.A.ci + e);
-    if (VALS) av = __ldg(a.A.val + e);
-    const int64_t bs = __ldg(a.B.rp + j);
-    len = (int)(__ldg(a.B.rp + j + 1) - bs);
-    pc += bs;
-    pv += bs;
-  }
-  m.pc[w][lane] = pc;
-  m.pv[w][lane] = pv;
-  m.len[w][lane] = len;
-  m.av[w][lane] = av;
-  __syncwarp();
-  return (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
-}
-
-template <int LOG2S>
-__device__ __forceinline__ unsigned hslot(int c) {
-  return ((unsigned)c * 0x9E3779B1u) >> (32 - LOG2S);
-}
-
-// insert c (if act) into keys[]: warp-uniform probing rounds; returns the slot
-template <int LOG2S>
-__device__ __forceinline__ unsigned warp_insert(int* keys, int c, bool act, int& inserted) {
-  constexpr unsigned MASK = (1u << LOG2S) - 1;
-  unsigned h = hslot<LOG2S>(c);
-  int k = keys[h];
-  // fast path, straight-line: a new key claims its empty home slot with one CAS
-  const int claim = act && k == kEmptyKey;
-  int pend = act && k != c;
-  if (__any_sync(0xffffffffu, claim)) {
-    if (claim) {
-      const int old = atomicCAS(&keys[h], kEmptyKey, c);
-      if (old == kEmptyKey || old == c) {
-        inserted += old == kEmptyKey;
-        pend = 0;
-      } else {
-        k = old;  // lost to another column of this instruction: probe on
-      }
-    }
-  }
-  // slow path: home slot held by another column (probe linearly)
-  while (__any_sync(0xffffffffu, pend)) {
-    if (pend) {
-      if (k == c) {
-        pend = 0;
-      } else if (k == kEmptyKey) {
-        const int old = atomicCAS(&keys[h], kEmptyKey, c);
-        if (old == kEmptyKey || old == c) {
-          inserted += old == kEmptyKey;
-          pend = 0;
-        } else {
-          k = old;
-        }
-      } else {
-        h = (h + 1) & MASK;
-        k = *(volatile int*)&keys[h];
-      }
-    }
-  }
-  return h;
-}
-
-template <int LOG2S, int NW, int MODE>
-__global__ void __launch_bounds__(NW * 32) k_warp_hash(Stage3Args a) {
-  constexpr bool FILL = MODE == MODE_FILL;
-  constexpr bool SORTED = MODE != MODE_COUNT;
-  constexpr int S = 1 << LOG2S;
-  constexpr unsigned MASK = S - 1;
-  constexpr int SHIFT = 32 - LOG2S;
-  __shared__ int s_keys[NW][S];
-  __shared__ int s_scratch[SORTED ? NW : 1][SORTED ? S : 1];
-  __shared__ double s_vals[FILL ? NW : 1][FILL ? S : 1];
-  __shared__ WarpMeta<NW> meta;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int* keys = s_keys[w];
-
-  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
-    const int row = __ldg(a.perm + a.first + r);
-    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-#pragma unroll 4
-    for (int s = lane; s < S; s += 32) {
-      keys[s] = kEmptyKey;
-      if (FILL) s_vals[w][s] = -0.0;  // -0.0 + x == x: the first add is "c_ik <- value"
-    }
-    int inserted = 0;
-    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
-      const int nE = stage_a_chunk<NW, FILL>(a, meta, w, lane, e0, a1);
-      int c0 = kEmptyKey, c1 = kEmptyKey;
-      double v0 = 0.0, v1 = 0.0;
-      if (lane < meta.len[w][0]) {
-        c0 = __ldg(meta.pc[w][0] + lane);
-        if (FILL) v0 = __ldg(meta.pv[w][0] + lane);
-      }
-      if (nE > 1 && lane < meta.len[w][1]) {
-        c1 = __ldg(meta.pc[w][1] + lane);
-        if (FILL) v1 = __ldg(meta.pv[w][1] + lane);
-      }
-      for (int t = 0; t < nE; ++t) {
-        int c2 = kEmptyKey;
-        double v2 = 0.0;
-        if (t + 2 < nE && lane < meta.len[w][t + 2]) {
-          c2 = __ldg(meta.pc[w][t + 2] + lane);
-          if (FILL) v2 = __ldg(meta.pv[w][t + 2] + lane);
-        }
-        const int lt = meta.len[w][t];
-        const unsigned h = warp_insert<LOG2S>(keys, c0, lane < lt, inserted);  // lines 7-8
-        if (FILL) {
-          __syncwarp();
-          if (lane < lt) s_vals[w][h] = __dadd_rn(s_vals[w][h], __dmul_rn(meta.av[w][t], v0));
-        }
-        if (lt > 32) {  // rest of a long b_j*, 32 columns per instruction
-          for (int q0 = 32; q0 < lt; q0 += 32) {
-            const bool act = q0 + lane < lt;
-            const int c = act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey;
-            const unsigned hh = warp_insert<LOG2S>(keys, c, act, inserted);
-            if (FILL) {
-              const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
-              __syncwarp();
-              if (act) s_vals[w][hh] = __dadd_rn(s_vals[w][hh], __dmul_rn(meta.av[w][t], v));
-            }
-          }
-        }
-        c0 = c1;
-        v0 = v1;
-        c1 = c2;
-        v1 = v2;
-      }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
-    if (!SORTED) {
-      if (lane == 0 && a.nnz_row) a.nnz_row[row] = inserted;
-      __syncwarp();
-      continue;
-    }
-    const int cnt = inserted;
-    int* scratch = s_scratch[SORTED ? w : 0];
-    int base = 0;
-#pragma unroll 4
-    for (int s0 = 0; s0 < S; s0 += 32) {
-      const int kk = keys[s0 + lane];
-      const bool occ = kk != kEmptyKey;
-      const unsigned bal = __ballot_sync(0xffffffffu, occ);
-      if (occ) scratch[base + __popc(bal & lanemask_lt())] = kk;
-      base += __popc(bal);
-    }
-    __syncwarp();
-    const int64_t o = __ldg(a.out_off + row);
-    warp_emit_sorted<FILL>(keys, FILL ? s_vals[FILL ? w : 0] : nullptr, scratch, cnt, MASK, SHIFT, lane,
-                           a.out_col + o, FILL ? a.out_val + o : nullptr);
-    if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
-    __syncwarp();
-  }
-}
-
-// PRECISE numeric, warp classes: the symbolic pass (STRUCT) left the row's sorted column set
-// at struct_col + struct_off[row].  Build a read-only key -> position table, accumulate each
-// product into vals[position] (positions are distinct within one b_j*; j-ascending order
-// across them: the oracle's order) and write C's row in order: no insertion, no sort.
-template <int LOG2S, int NW>
-__global__ void __launch_bounds__(NW * 32) k_warp_dense(Stage3Args a) {
-  constexpr int S = 1 << LOG2S;
-  constexpr unsigned MASK = S - 1;
-  __shared__ int2 s_tab[NW][S];
-  __shared__ double s_vals[NW][S / 2];
-  __shared__ WarpMeta<NW> meta;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int2* tab = s_tab[w];
-  double* vals = s_vals[w];
-
-  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
-    const int row = __ldg(a.perm + a.first + r);
-    const int64_t o = __ldg(a.out_off + row);
-    const int nnz = (int)(__ldg(a.out_off + row + 1) - o);
-    const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
-#pragma unroll 4
-    for (int s = lane; s < S; s += 32) tab[s].x = kEmptyKey;
-    for (int p = lane; p < nnz; p += 32) vals[p] = -0.0;  // identity of +: first add == line 9
-    __syncwarp();
-    for (int p = lane; p < nnz; p += 32) {
-      const int c = __ldg(sc + p);
-      a.out_col[o + p] = c;  // C's columns: the sorted set itself
-      unsigned h = hslot<LOG2S>(c);
-      while (atomicCAS(&tab[h].x, kEmptyKey, c) != kEmptyKey) h = (h + 1) & MASK;
-      tab[h].y = p;
-    }
-    __syncwarp();
-    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
-      const int nE = stage_a_chunk<NW, true>(a, meta, w, lane, e0, a1);
-      int c0 = kEmptyKey, c1 = kEmptyKey;
-      double v0 = 0.0, v1 = 0.0;
-      if (lane < meta.len[w][0]) {
-        c0 = __ldg(meta.pc[w][0] + lane);
-        v0 = __ldg(meta.pv[w][0] + lane);
-      }
-      if (nE > 1 && lane < meta.len[w][1]) {
-        c1 = __ldg(meta.pc[w][1] + lane);
-        v1 = __ldg(meta.pv[w][1] + lane);
-      }
-      for (int t = 0; t < nE; ++t) {
-        int c2 = kEmptyKey;
-        double v2 = 0.0;
-        if (t + 2 < nE && lane < meta.len[w][t + 2]) {
-          c2 = __ldg(meta.pc[w][t + 2] + lane);
-          v2 = __ldg(meta.pv[w][t + 2] + lane);
-        }
-        const int lt = meta.len[w][t];
-        const double at = meta.av[w][t];
-        {
-          const bool act = lane < lt;
-          unsigned h = hslot<LOG2S>(c0);
-          int2 kv = tab[h];
-          bool pend = act && kv.x != c0;
-          while (__any_sync(0xffffffffu, pend)) {
-            if (pend) {
-              h = (h + 1) & MASK;
-              kv = tab[h];
-              pend = kv.x != c0;
-            }
-          }
-          __syncwarp();
-          if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v0));  // line 11
-        }
-        if (lt > 32) {
-          for (int q0 = 32; q0 < lt; q0 += 32) {
-            const bool act = q0 + lane < lt;
-            const int c = act ? __ldg(meta.pc[w][t] + q0 + lane) : kEmptyKey;
-            const double v = act ? __ldg(meta.pv[w][t] + q0 + lane) : 0.0;
-            unsigned h = hslot<LOG2S>(c);
-            int2 kv = tab[h];
-            bool pend = act && kv.x != c;
-            while (__any_sync(0xffffffffu, pend)) {
-              if (pend) {
-                h = (h + 1) & MASK;
-                kv = tab[h];
-                pend = kv.x != c;
-              }
-            }
-            __syncwarp();
-            if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v));
-          }
-        }
-        c0 = c1;
-        v0 = v1;
-        c1 = c2;
-        v1 = v2;
-      }
-      __syncwarp();
-    }
-    for (int p = lane; p < nnz; p += 32) a.out_val[o + p] = vals[p];
-    __syncwarp();
   }
 }
 
@@ -783,6 +396,8 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
 // --------------------------------------------------------------- launch helpers
 int g_num_sms = 0;
 
+}  // namespace
+
 int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
@@ -792,6 +407,8 @@ int num_sms() {
   }
   return g_num_sms;
 }
+
+namespace {
 
 template <typename K>
 cudaError_t launch_persistent(K kernel, int nt, size_t dsmem, int64_t work_units, int units_per_block,
@@ -830,35 +447,14 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_G32: SG_GROUP(32, 8);
 #undef SG_GROUP
     case T_W64:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<6, 8>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<6, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<6, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
-      return launch_persistent(k_warp_hash<6, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
     case T_W128:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<7, 8>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<7, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<7, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
-      return launch_persistent(k_warp_hash<7, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
     case T_W256:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<8, 8>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<8, 8, MODE_FILL>, 256, 0, a.count, 8, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<8, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
-      return launch_persistent(k_warp_hash<8, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
     case T_W512:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<9, 4>, 128, 0, a.count, 4, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<9, 4, MODE_FILL>, 128, 0, a.count, 4, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<9, 8, MODE_STRUCT>, 256, 0, a.count, 8, a, s);
-      return launch_persistent(k_warp_hash<9, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
     case T_W1024:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<10, 2>, 64, 0, a.count, 2, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<10, 2, MODE_FILL>, 64, 0, a.count, 2, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<10, 4, MODE_STRUCT>, 128, 0, a.count, 4, a, s);
-      return launch_persistent(k_warp_hash<10, 8, MODE_COUNT>, 256, 0, a.count, 8, a, s);
     case T_W2048:
-      if (a.mode == MODE_DENSE) return launch_persistent(k_warp_dense<11, 1>, 32, 0, a.count, 1, a, s);
-      if (a.mode == MODE_FILL) return launch_persistent(k_warp_hash<11, 1, MODE_FILL>, 32, 0, a.count, 1, a, s);
-      if (a.mode == MODE_STRUCT) return launch_persistent(k_warp_hash<11, 2, MODE_STRUCT>, 64, 0, a.count, 2, a, s);
-      return launch_persistent(k_warp_hash<11, 4, MODE_COUNT>, 128, 0, a.count, 4, a, s);
+      return launch_warp_tier(tier, a, s);
+    case T_BW:
+      return launch_bw_tier(a, s);
     // bucket ESC for values; counting only needs distinct keys: the CTA hash of the same size
     case T_E2048:
       if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * 4, a.count, 1, a, s);

@@ -1,0 +1,681 @@
+// warp.cu — stage 3, warp classes w64..w2048: one warp per row, an S-slot shared-memory
+// hash ("computing the resulting matrix", [P:262-284]; Algorithm 1 lines 3-11 [P:121-135]).
+//
+// Lanes walk the rows b_j* of the row's a_ij in j-ascending order, one b_j* (up to 32 of its
+// entries) per instruction.  Columns inside one b_j* are distinct, so no two lanes of one
+// instruction insert or accumulate into one slot: the values of a column are added in
+// j-ascending order from the identity -0.0, i.e. the oracle's rounding (R1),
+// deterministic and without value atomics.
+//
+// The loads of four consecutive b_j* are issued before their inserts (memory-level
+// parallelism of 4 per warp); rows whose chunk holds a b_j* longer than 32 take a generic
+// loop with the same order.  New keys are appended to a per-warp list as they are claimed,
+// so the sorted output needs no compaction pass over the table.
+//
+//   MODE_COUNT   insert keys, count                              (precise symbolic)
+//   MODE_STRUCT  insert keys, count, emit the sorted key set     (precise symbolic)
+//   MODE_FILL    insert + accumulate, emit the sorted row         (hybrid: C~)
+//   MODE_DENSE   precise numeric: look columns up in a read-only key -> position table built
+//                from the STRUCT set; accumulate into a dense array already in column order.
+#include <climits>
+
+#include "common.cuh"
+
+namespace sg {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt_() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <int LOG2S>
+__device__ __forceinline__ unsigned whash(int c) {
+  return ((unsigned)c * 0x9E3779B1u) >> (32 - LOG2S);
+}
+
+// Insert c (if act) into keys; a lane that claims a new slot appends c to list.  Returns the
+// slot.  Warp-uniform probing rounds; the common case (found at home) is one LDS + one vote.
+template <int LOG2S, bool LIST>
+__device__ __forceinline__ unsigned winsert(int* keys, int* list, int& cnt, int c, bool act) {
+  constexpr unsigned MASK = (1u << LOG2S) - 1;
+  volatile int* vk = keys;
+  unsigned h = whash<LOG2S>(c);
+  int k = vk[h];
+  bool pend = act && k != c;
+  while (true) {
+    bool claimed = false;
+    if (pend) {
+      if (k == kEmptyKey) {
+        const int old = atomicCAS(&keys[h], kEmptyKey, c);
+        if (old == kEmptyKey) {
+          claimed = true;
+          pend = false;
+        } else if (old == c) {
+          pend = false;
+        } else {
+          h = (h + 1) & MASK;
+          k = vk[h];
+          pend = k != c;
+        }
+      } else {
+        h = (h + 1) & MASK;
+        k = vk[h];
+        pend = k != c;
+      }
+    }
+    const unsigned cb = __ballot_sync(kFull, claimed);
+    if (cb) {
+      if (LIST && claimed) list[cnt + __popc(cb & lanemask_lt_())] = c;
+      cnt += __popc(cb);
+    }
+    if (!__any_sync(kFull, pend)) break;
+  }
+  return h;
+}
+
+// Read-only lookup of a key that is known to be present.
+template <int LOG2S>
+__device__ __forceinline__ int2 wlookup(const int2* tab, int c, bool act) {
+  constexpr unsigned MASK = (1u << LOG2S) - 1;
+  unsigned h = whash<LOG2S>(c);
+  int2 kv = tab[h];
+  bool pend = act && kv.x != c;
+  while (__any_sync(kFull, pend)) {
+    if (pend) {
+      h = (h + 1) & MASK;
+      kv = tab[h];
+      pend = kv.x != c;
+    }
+  }
+  return kv;
+}
+
+// Register bitonic sort of N = 32·E int keys in "blocked" layout (lane l holds l·E .. l·E+E-1).
+template <int E>
+__device__ __forceinline__ void bitonic_blocked(int (&k)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const bool asc = ((lane * E + r) & kk) == 0;
+          const int p = __shfl_xor_sync(kFull, k[r], lj);
+          k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (r & j) continue;
+          const bool asc = ((lane * E + r) & kk) == 0;
+          const int x = k[r], y = k[r | j];
+          k[r] = asc ? min(x, y) : max(x, y);
+          k[r | j] = asc ? max(x, y) : min(x, y);
+        }
+      }
+    }
+  }
+}
+
+// Sort list[0, cnt) ascending in place (registers for cnt <= 128, shared-memory bitonic above;
+// list must have room for the next power of two).
+__device__ __forceinline__ void warp_sort_list(int* list, int cnt, int lane) {
+  if (cnt <= 32) {
+    int k[1];
+    k[0] = lane < cnt ? list[lane] : INT_MAX;
+    bitonic_blocked<1>(k, lane);
+    __syncwarp();
+    if (lane < cnt) list[lane] = k[0];
+  } else if (cnt <= 64) {
+    int k[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) k[r] = lane * 2 + r < cnt ? list[lane * 2 + r] : INT_MAX;
+    bitonic_blocked<2>(k, lane);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (lane * 2 + r < cnt) list[lane * 2 + r] = k[r];
+  } else if (cnt <= 128) {
+    int k[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) k[r] = lane * 4 + r < cnt ? list[lane * 4 + r] : INT_MAX;
+    bitonic_blocked<4>(k, lane);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (lane * 4 + r < cnt) list[lane * 4 + r] = k[r];
+  } else {
+    int N = 1;
+    while (N < cnt) N <<= 1;
+    for (int s = cnt + lane; s < N; s += 32) list[s] = INT_MAX;
+    __syncwarp();
+    for (int kk = 2; kk <= N; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < (N >> 1); i += 32) {
+          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          const int hi = lo + j;
+          const bool asc = (lo & kk) == 0;
+          const int kl = list[lo], kh = list[hi];
+          if ((kl > kh) == asc) {
+            list[lo] = kh;
+            list[hi] = kl;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// One a_ij chunk (up to 32 entries of row i of A): lane e holds b_j*'s start and length and a_ij.
+// IT: index type of B's entries (int32_t when nnz(B) < 2^31: one shuffle and one IMAD.WIDE per
+// address instead of 64-bit arithmetic).
+template <typename IT>
+struct AChunk {
+  IT bs;
+  int len;
+  double av;
+};
+
+template <bool VALS, typename IT>
+__device__ __forceinline__ AChunk<IT> load_achunk(const Stage3Args& a, int64_t e, int64_t a1) {
+  AChunk<IT> ch{0, 0, 0.0};
+  if (e < a1) {
+    const int j = __ldg(a.A.ci + e);
+    if (VALS) ch.av = __ldg(a.A.val + e);
+    const int64_t b0 = __ldg(a.B.rp + j);
+    ch.bs = (IT)b0;
+    ch.len = (int)(__ldg(a.B.rp + j + 1) - b0);
+  }
+  return ch;
+}
+
+constexpr int kGroup = 4;  // b_j* whose loads are in flight together
+
+// Walk all products of row i in Algorithm-1 order, calling op(c, v, at, act) once per b_j*
+// segment of up to 32 entries (c: this lane's column, v: b_jk, at: a_ij).
+template <bool VALS, typename IT, typename Op>
+__device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_t a1, int lane, Op&& op) {
+  for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+    const AChunk<IT> ch = load_achunk<VALS, IT>(a, e0 + lane, a1);
+    const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+    if (!__any_sync(kFull, ch.len > 32)) {
+      for (int t0 = 0; t0 < nE; t0 += kGroup) {
+        int c[kGroup];
+        double v[kGroup], at[kGroup];
+        bool act[kGroup];
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          const int t = t0 + u;  // <= 31; lanes past the chunk have len 0
+          const IT q = __shfl_sync(kFull, ch.bs, t) + (IT)lane;
+          const int len = __shfl_sync(kFull, ch.len, t);
+          act[u] = lane < len;
+          c[u] = act[u] ? __ldg(a.B.ci + q) : kEmptyKey;
+          if (VALS) {
+            at[u] = __shfl_sync(kFull, ch.av, t);
+            v[u] = act[u] ? __ldg(a.B.val + q) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u)
+          if (t0 + u < nE) op(c[u], VALS ? v[u] : 0.0, VALS ? at[u] : 0.0, act[u]);
+      }
+    } else {
+      for (int t = 0; t < nE; ++t) {
+        const IT bs = __shfl_sync(kFull, ch.bs, t);
+        const int len = __shfl_sync(kFull, ch.len, t);
+        const double at = VALS ? __shfl_sync(kFull, ch.av, t) : 0.0;
+        for (int q0 = 0; q0 < len; q0 += 32) {
+          const bool act = q0 + lane < len;
+          const IT q = bs + (IT)(q0 + lane);
+          const int c = act ? __ldg(a.B.ci + q) : kEmptyKey;
+          const double v = (VALS && act) ? __ldg(a.B.val + q) : 0.0;
+          op(c, v, at, act);
+        }
+      }
+    }
+  }
+}
+
+// COUNT / STRUCT / FILL.  Shared memory per warp: keys[S], list[S], FILL: vals[S].
+template <int LOG2S, int NW, int MODE, typename IT>
+__global__ void __launch_bounds__(NW * 32) k_wrow(Stage3Args a) {
+  constexpr bool FILL = MODE == MODE_FILL;
+  constexpr bool LIST = MODE != MODE_COUNT;
+  constexpr int S = 1 << LOG2S;
+  __shared__ __align__(16) int s_keys[NW][S];
+  __shared__ __align__(16) int s_list[LIST ? NW : 1][LIST ? S : 1];
+  __shared__ __align__(16) double s_vals[FILL ? NW : 1][FILL ? S : 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int* keys = s_keys[w];
+  int* list = s_list[LIST ? w : 0];
+  double* vals = s_vals[FILL ? w : 0];
+
+  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int4* k4 = reinterpret_cast<int4*>(keys);
+#pragma unroll
+    for (int s = lane; s < S / 4; s += 32) k4[s] = make_int4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
+    if (FILL) {
+      double2* v2 = reinterpret_cast<double2*>(vals);
+#pragma unroll
+      for (int s = lane; s < S / 2; s += 32) v2[s] = make_double2(-0.0, -0.0);  // -0.0 + x == x
+    }
+    __syncwarp();
+    int cnt = 0;
+    walk_row<FILL, IT>(a, a0, a1, lane, [=, &cnt](int c, double v, double at, bool act) {
+      const unsigned h = winsert<LOG2S, LIST>(keys, list, cnt, c, act);  // lines 7-8 / 10
+      if (FILL) {
+        if (act) vals[h] = __dadd_rn(vals[h], __dmul_rn(at, v));  // lines 6, 9, 11
+        __syncwarp();
+      }
+    });
+    __syncwarp();
+    if (MODE == MODE_COUNT) {
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+      __syncwarp();
+      continue;
+    }
+    warp_sort_list(list, cnt, lane);
+    const int64_t o = __ldg(a.out_off + row);
+    for (int t = lane; t < cnt; t += 32) {
+      const int c = list[t];
+      a.out_col[o + t] = c;
+      if (FILL) {
+        constexpr unsigned MASK = S - 1;
+        unsigned h = whash<LOG2S>(c);
+        while (keys[h] != c) h = (h + 1) & MASK;
+        a.out_val[o + t] = vals[h];
+      }
+    }
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+    __syncwarp();
+  }
+}
+
+// PRECISE numeric: the sorted column set of row i is at struct_col + struct_off[i].
+template <int LOG2S, int NW, typename IT>
+__global__ void __launch_bounds__(NW * 32) k_wdense(Stage3Args a) {
+  constexpr int S = 1 << LOG2S;
+  constexpr unsigned MASK = S - 1;
+  __shared__ __align__(16) int2 s_tab[NW][S];
+  __shared__ __align__(16) double s_vals[NW][S / 2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int2* tab = s_tab[w];
+  double* vals = s_vals[w];
+
+  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int64_t o = __ldg(a.out_off + row);
+    const int nnz = (int)(__ldg(a.out_off + row + 1) - o);
+    const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
+    int4* t4 = reinterpret_cast<int4*>(tab);
+#pragma unroll
+    for (int s = lane; s < S / 2; s += 32) t4[s] = make_int4(kEmptyKey, 0, kEmptyKey, 0);
+    for (int p = lane; p < nnz; p += 32) vals[p] = -0.0;  // identity of +: first add == line 9
+    __syncwarp();
+    for (int p = lane; p < nnz; p += 32) {
+      const int c = __ldg(sc + p);
+      a.out_col[o + p] = c;  // C's columns: the sorted set itself
+      unsigned h = whash<LOG2S>(c);
+      while (atomicCAS(&tab[h].x, kEmptyKey, c) != kEmptyKey) h = (h + 1) & MASK;
+      tab[h].y = p;
+    }
+    __syncwarp();
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
+      const int2 kv = wlookup<LOG2S>(tab, c, act);
+      if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v));  // line 11
+      __syncwarp();
+    });
+    __syncwarp();
+    for (int p = lane; p < nnz; p += 32) a.out_val[o + p] = vals[p];
+    __syncwarp();
+  }
+}
+
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += x;
+  }
+  return v;
+}
+
+// ----------------------------------------------------------------------------------------
+// T_BW: the sparse accumulator of Gilbert et al. ([P:142], the dense vector of Algorithm 1's
+// "insert/accumulate") restricted to the row's column window [lo, lo + W): bit d of the
+// warp's bitmap stands for column lo + d, one summary bit per bitmap word.  Inserting is one
+// shared-memory OR per product (no probing, no votes); the row comes out ordered by scanning
+// only the nonzero words; a column's position in the row is the popcount rank of its bit.
+//
+// Per-warp dynamic shared memory (32-bit words): bm[nwd] | sm[nsw] | FILL: pre[nwd/2] (uint16
+// rank of each nonzero word's first bit) | lst[nvp] (nonzero words, ascending) | vals[nv].
+//   COUNT  one pass over the products, popcounts of the nonzero words (precise symbolic)
+//   FILL   pass 1 sets the bits; ranks and columns from the nonzero words; pass 2 adds each
+//          product into vals[rank] (j-ascending per column: the oracle's order) and the row
+//          is written in order with no sort (precise numeric into C, hybrid into C~)
+// The bitmap is zero between rows: every row clears the words it set.
+// 32-bit shared-window addressing (the per-warp regions are carved from dynamic shared memory;
+// explicit ld/st/atom.shared keep every access a direct LDS/STS/ATOMS).
+__device__ __forceinline__ unsigned sh_atom_or(unsigned addr, unsigned v) {
+  unsigned r;
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sh_red_or(unsigned addr, unsigned v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned sh_ld(unsigned addr) {
+  unsigned r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sh_st(unsigned addr, unsigned v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned sh_ld_u16(unsigned addr) {
+  unsigned short r;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sh_st_u16(unsigned addr, unsigned v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ double sh_ld_f64(unsigned addr) {
+  double r;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sh_st_f64(unsigned addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ int4 sh_ld_v4(unsigned addr) {
+  int4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
+}
+
+// Per-warp shared-memory layout of the window class (byte offsets from the warp's base):
+//   bm   uint32[nwd]   window bitmap                           (all modes)
+//   sm   uint32[nsw]   summary bits (a bit per bm word)        (STRUCT, FILL)
+//   pre  uint16[nwd]   rank of each nonzero word's first bit    (FILL, DENSE)
+//   lst  int32[nvp]    nonzero words, ascending                 (STRUCT, FILL)
+//   vals double[nv]    the row's values in column order         (FILL, DENSE)
+struct BwLayout {
+  int nwd, nsw, nvp, nv;
+  unsigned o_sm, o_pre, o_lst, o_vals, bytes;  // per warp, bytes is a multiple of 16
+};
+
+__host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vmax) {
+  BwLayout L;
+  L.nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
+  L.nsw = (L.nwd / 32 + 31) / 32 * 32;
+  L.nv = (int)(vmax > 0 ? vmax : 1);
+  L.nvp = (L.nv + 3) & ~3;
+  const bool summ = mode == MODE_STRUCT || mode == MODE_FILL;
+  const bool vals = mode == MODE_FILL || mode == MODE_DENSE;
+  unsigned off = 4u * L.nwd;
+  L.o_sm = off;
+  if (summ) off += 4u * L.nsw;
+  L.o_pre = off;
+  if (vals) off += 2u * L.nwd;
+  L.o_lst = off;
+  if (summ) off += 4u * L.nvp;
+  L.o_vals = off;
+  if (vals) off += 8u * L.nv;
+  L.bytes = (off + 15u) & ~15u;
+  return L;
+}
+
+template <int MODE, typename IT>
+__global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
+  constexpr bool SUMM = MODE == MODE_STRUCT || MODE == MODE_FILL;  // products -> bits + summary
+  constexpr bool VALS = MODE == MODE_FILL || MODE == MODE_DENSE;
+  extern __shared__ __align__(16) uint32_t s_bw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nwd = L.nwd, nsw = L.nsw;
+  // byte addresses in the shared window
+  const unsigned bm = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
+  const unsigned sm = bm + L.o_sm, pre = bm + L.o_pre, lst = bm + L.o_lst, vals = bm + L.o_vals;
+  for (unsigned i = lane; i < (L.o_pre + 15u) / 16u; i += 32) sh_st_v4_zero(bm + 16u * i);  // bm (+ sm)
+  __syncwarp();
+
+  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < a.count; r += int64_t(gridDim.x) * nw) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    const int64_t o = __ldg(a.out_off + row);
+    int nnz = 0;
+    if (MODE != MODE_DENSE) {
+      // lines 7-8 / 10 of Algorithm 1 for every product: set the column's bit.  With the
+      // summary: only the lane that finds a word empty sets its summary bit, so summary
+      // atomics are rare and seldom share an address.
+      walk_row<false, IT>(a, a0, a1, lane, [=](int c, double, double, bool act) {
+        if (act) {
+          const unsigned d = (unsigned)(c - lo);
+          const unsigned wa = bm + ((d >> 5) << 2);
+          if (SUMM) {
+            if (sh_atom_or(wa, 1u << (d & 31)) == 0u) sh_red_or(sm + ((d >> 10) << 2), 1u << ((d >> 5) & 31));
+          } else {
+            sh_red_or(wa, 1u << (d & 31));
+          }
+        }
+      });
+      __syncwarp();
+    }
+    if (MODE == MODE_COUNT) {
+      // popcount of the window, clearing the words that were set
+      int cnt = 0;
+      for (int q = lane; q < nwd / 4; q += 32) {
+        const int4 x = sh_ld_v4(bm + 16u * q);
+        if ((x.x | x.y | x.z | x.w) != 0) {
+          cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+          sh_st_v4_zero(bm + 16u * q);
+        }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
+      __syncwarp();
+      continue;
+    }
+    int nl = 0;
+    if (SUMM) {
+      // nonzero words in ascending order (clears the summary)
+      for (int s0 = 0; s0 < nsw; s0 += 32) {
+        const int s = s0 + lane;
+        unsigned sw = sh_ld(sm + 4u * s);
+        if (sw) sh_st(sm + 4u * s, 0u);
+        const int pc = __popc(sw);
+        const int inc = warp_incl_scan(pc, lane);
+        int pos = nl + inc - pc;
+        while (sw) {
+          sh_st(lst + 4u * pos++, unsigned(s * 32 + __ffs(sw) - 1));
+          sw &= sw - 1;
+        }
+        nl += __shfl_sync(kFull, inc, 31);
+      }
+      __syncwarp();
+      // ranks of the nonzero words; the row's columns in order (no sort)
+      int32_t* oc = a.out_col + o;
+      for (int q0 = 0; q0 < nl; q0 += 32) {
+        const int q = q0 + lane;
+        const int wd = q < nl ? (int)sh_ld(lst + 4u * q) : 0;
+        unsigned word = q < nl ? sh_ld(bm + 4u * wd) : 0u;
+        const int pc = __popc(word);
+        const int inc = warp_incl_scan(pc, lane);
+        int p = nnz + inc - pc;
+        if (VALS && q < nl) sh_st_u16(pre + 2u * wd, (unsigned)p);
+        const int cb = lo + wd * 32;
+        while (word) {
+          oc[p++] = cb + __ffs(word) - 1;
+          word &= word - 1;
+        }
+        nnz += __shfl_sync(kFull, inc, 31);
+      }
+    }
+    if (MODE == MODE_STRUCT) {
+      for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+      __syncwarp();
+      continue;
+    }
+    const int32_t* sc = nullptr;
+    if (MODE == MODE_DENSE) {
+      // the sorted column set from the symbolic pass: bits, ranks and C's columns directly
+      nnz = (int)(__ldg(a.out_off + row + 1) - o);
+      sc = a.struct_col + __ldg(a.struct_off + row);
+      for (int p0 = 0; p0 < nnz; p0 += 32) {
+        const int p = p0 + lane;
+        const int c = p < nnz ? __ldg(sc + p) : 0;
+        const int cprev0 = (p0 > 0 && lane == 0) ? __ldg(sc + p - 1) : 0;
+        int cprev = __shfl_up_sync(kFull, c, 1);
+        if (lane == 0) cprev = cprev0;
+        if (p < nnz) {
+          a.out_col[o + p] = c;
+          const unsigned d = (unsigned)(c - lo);
+          sh_red_or(bm + ((d >> 5) << 2), 1u << (d & 31));
+          if (p == 0 || (((unsigned)(cprev - lo)) >> 5) != (d >> 5)) sh_st_u16(pre + 2u * (d >> 5), (unsigned)p);
+        }
+      }
+    }
+    for (int p = lane; p < nnz; p += 32) sh_st_f64(vals + 8u * p, -0.0);  // identity of +: first add == line 9
+    __syncwarp();
+    // lines 6, 9, 11: c_ik += a_ij b_jk at the column's rank
+    walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
+      if (act) {
+        const unsigned d = (unsigned)(c - lo);
+        const unsigned wd = d >> 5;
+        const unsigned rank = sh_ld_u16(pre + 2u * wd) + __popc(sh_ld(bm + 4u * wd) & ((1u << (d & 31)) - 1u));
+        const unsigned va = vals + 8u * rank;
+        sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
+      }
+      __syncwarp();
+    });
+    __syncwarp();
+    double* ov = a.out_val + o;
+    for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
+    if (MODE == MODE_FILL) {
+      for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
+    } else {
+      for (int p = lane; p < nnz; p += 32) sh_st(bm + 4u * ((unsigned)(__ldg(sc + p) - lo) >> 5), 0u);
+    }
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+template <typename K>
+static cudaError_t launch_warp_kernel(K kernel, int nw, int64_t rows, const Stage3Args& a, cudaStream_t s) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nw * 32, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (rows + nw - 1) / nw;
+  const int64_t cap = int64_t(num_sms()) * per_sm * 4;
+  int64_t grid = need < cap ? need : cap;
+  if (grid < 1) grid = 1;
+  kernel<<<(unsigned)grid, nw * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Warp classes T_W64..T_W2048: S = 64 << (tier - T_W64) slots.  Warps per block: as many as
+// the 48 KB static shared-memory limit allows (per warp: COUNT 4S, STRUCT 8S, FILL 16S,
+// DENSE 12S bytes), at most 8.
+cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s) {
+  const bool i32 = a.b_nnz < (int64_t(1) << 31);
+#define SG_NW(BYTES) ((49152 / (BYTES)) < 8 ? (49152 / (BYTES)) : 8)
+#define SG_W(LOG2S)                                                                           \
+  {                                                                                           \
+    constexpr int S_ = 1 << LOG2S;                                                            \
+    constexpr int NC = SG_NW(4 * S_), NS = SG_NW(8 * S_), NF = SG_NW(16 * S_), ND = SG_NW(12 * S_); \
+    if (i32) {                                                                                \
+      switch (a.mode) {                                                                       \
+        case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int>, ND, a.count, a, s); \
+        case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int>, NF, a.count, a, s); \
+        case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int>, NS, a.count, a, s); \
+        default: return launch_warp_kernel(k_wrow<LOG2S, NC, MODE_COUNT, int>, NC, a.count, a, s); \
+      }                                                                                       \
+    }                                                                                         \
+    switch (a.mode) {                                                                         \
+      case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int64_t>, ND, a.count, a, s); \
+      case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int64_t>, NF, a.count, a, s); \
+      case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int64_t>, NS, a.count, a, s); \
+      default: return launch_warp_kernel(k_wrow<LOG2S, NC, MODE_COUNT, int64_t>, NC, a.count, a, s); \
+    }                                                                                         \
+  }
+  switch (tier) {
+    case T_W64: SG_W(6)
+    case T_W128: SG_W(7)
+    case T_W256: SG_W(8)
+    case T_W512: SG_W(9)
+    case T_W1024: SG_W(10)
+    case T_W2048: SG_W(11)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SG_W
+#undef SG_NW
+}
+
+// T_BW launch: shared memory sized by the class's largest window and row length; warps per
+// block chosen for the most resident warps per SM.
+template <int MODE>
+static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
+  const BwLayout L = bw_layout(MODE, a.bw_wmax, a.bw_vmax);
+  const bool i32 = a.b_nnz < (int64_t(1) << 31);
+  auto kern = i32 ? k_bwrow<MODE, int> : k_bwrow<MODE, int64_t>;
+  int best_nw = 1, best_warps = 0;
+  for (int nw = 8; nw >= 1; nw >>= 1) {
+    const size_t bytes = size_t(nw) * L.bytes;
+    if (bytes > 227 * 1024) continue;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, bytes);
+    if (e != cudaSuccess) return e;
+    if (per_sm * nw > best_warps) {
+      best_warps = per_sm * nw;
+      best_nw = nw;
+    }
+  }
+  if (best_warps == 0) return cudaErrorInvalidConfiguration;
+  const size_t bytes = size_t(best_nw) * L.bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t need = (a.count + best_nw - 1) / best_nw;
+  const int64_t cap = int64_t(num_sms()) * (best_warps / best_nw);
+  const int64_t grid = need < cap ? need : cap;
+  kern<<<(unsigned)grid, best_nw * 32, bytes, s>>>(a, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  switch (a.mode) {
+    case MODE_FILL: return launch_bw_mode<MODE_FILL>(a, s);
+    case MODE_STRUCT: return launch_bw_mode<MODE_STRUCT>(a, s);
+    case MODE_DENSE: return launch_bw_mode<MODE_DENSE>(a, s);
+    default: return launch_bw_mode<MODE_COUNT>(a, s);
+  }
+}
+
+}  // namespace sg

@@ -75,7 +75,7 @@ def test_tier_boundaries(dup):
     assert np.all(np.diff(g["rp"]) <= g["u"])  # u_i >= nnz(c_i*) [S:211]
 
 
-def _classify(u, n):
+def _classify(u, n, W):
     """Python restatement of the stage-2 rule for the exact-integer check."""
     if u == 0:
         return 0
@@ -85,6 +85,8 @@ def _classify(u, n):
         while (1 << g) < u:
             g += 1
         return 1 + g
+    if 0 < W <= (1 << 17) and min(cap, W) <= 2048:   # window bitmap
+        return 19
     for t in range(7, 13):
         if 4 * (64 << (t - 7)) >= 5 * cap:
             return t
@@ -94,7 +96,21 @@ def _classify(u, n):
     for t in range(13, 16):
         if cap <= (2048 << (t - 13)):
             return t
-    return 19
+    return 20
+
+
+def _windows(A, B):
+    """W_i = max_j (last column of b_j*) - min_j (first column of b_j*) + 1 over the a_ij."""
+    W = np.zeros(A.shape[0], dtype=np.int64)
+    for i in range(A.shape[0]):
+        lo, hi = None, None
+        for j in A.ci[A.rp[i]:A.rp[i + 1]]:
+            if B.rp[j + 1] > B.rp[j]:
+                f, l = int(B.ci[B.rp[j]]), int(B.ci[B.rp[j + 1] - 1])
+                lo = f if lo is None else min(lo, f)
+                hi = l if hi is None else max(hi, l)
+        W[i] = 0 if lo is None else hi - lo + 1
+    return W
 
 
 def test_stage12_integers():
@@ -104,14 +120,15 @@ def test_stage12_integers():
     u, tot = oracle.upper_bound(A, B)
     np.testing.assert_array_equal(g["u"], u)
     assert g["stats"]["sum_u"] == tot
-    want = [_classify(int(x), B.shape[1]) for x in u]
+    W = _windows(A, B)
+    want = [_classify(int(x), B.shape[1], int(w)) for x, w in zip(u, W)]
     np.testing.assert_array_equal(g["tier"], np.array(want))
-    counts = np.bincount(np.array(want), minlength=20)
+    counts = np.bincount(np.array(want), minlength=21)
     from paper_1504_05022_b200 import TIER_NAMES
     assert g["stats"]["tier_rows"] == {TIER_NAMES[t]: int(c) for t, c in enumerate(counts) if c}
 
 
-@pytest.mark.parametrize("tier", list(range(1, 20)))
+@pytest.mark.parametrize("tier", list(range(1, 21)))
 def test_forced_tier(tier):
     """Every row that a class can hold is routed through it; results agree with the oracle
     (and so with every other class: P11 tier-forced agreement)."""
@@ -124,7 +141,7 @@ def test_forced_tier(tier):
     compare(g, R, exact=True, what="tier %d" % tier)
 
 
-@pytest.mark.parametrize("tier", [3, 6, 7, 9, 11, 12, 13, 15, 16, 17, 18, 19])
+@pytest.mark.parametrize("tier", [3, 6, 7, 9, 11, 12, 13, 15, 16, 17, 18, 19, 20])
 def test_forced_tier_precise(tier):
     """PRECISE strategy: symbolic (structure) and numeric (dense / bitmap) classes agree
     with the oracle when rows are forced through each class."""
