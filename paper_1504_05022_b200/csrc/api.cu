@@ -124,7 +124,7 @@ struct spgemm_handle_s {
   int64_t tier_count[NUM_TIERS] = {};
   int64_t tier_off[NUM_TIERS + 1] = {};
   int64_t sum_u = 0, max_u = 0, sum_cap = 0;
-  int64_t bw_wmax = 0, bw_vmax = 0;  // T_BW class: largest window, row length
+  int64_t bw_wmax = 0, bw_vmax = 0, bw_bmax = 0;  // T_BW class: largest window, row length, blocks
   bool sym_ok = false;
   int64_t nnz_c = 0;
   std::string err;
@@ -569,6 +569,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.rlo = ws.rlo;
     a.bw_wmax = h->bw_wmax;
     a.bw_vmax = h->bw_vmax;
+    a.bw_bmax_out = ws.summary + kSumBmax;
     cudaEventRecord(h->tev[t][0], h->stream);
     CK(h, launch_stage3_tier(t, a, h->stream));
     cudaEventRecord(h->tev[t][1], h->stream);
@@ -629,6 +630,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->nlong = h->tier_count[T_LONG];
     h->long_first = h->tier_off[T_LONG];
     h->bw_vmax = h->pinned[kSumVmax];  // exact: max nnz(c_i*) over the window rows
+    h->bw_bmax = h->pinned[kSumBmax];
     tr("re-binning");
   }
   h->sym_ok = true;
@@ -686,6 +688,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.rlo = h->ws.rlo;
         a.bw_wmax = h->bw_wmax;
         a.bw_vmax = h->bw_vmax;
+        a.bw_bmax = h->bw_bmax;
         cudaEventRecord(h->tev[t][0], h->stream);
         CK(h, launch_stage3_tier(t, a, h->stream));
         cudaEventRecord(h->tev[t][1], h->stream);

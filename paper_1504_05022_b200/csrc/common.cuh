@@ -169,6 +169,8 @@ struct Stage3Args {
   const int64_t* struct_off;  // DENSE: their per-row offsets
   const int32_t* rlo;         // T_BW: first column of each row's window
   int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
+  int64_t bw_bmax;            // T_BW numeric: most nonzero 1024-column blocks in a row
+  int64_t* bw_bmax_out;       // T_BW STRUCT: device max of the above (summary entry)
 };
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------
@@ -198,7 +200,8 @@ constexpr int kSumUMax = kSumU + 2;                // max u
 constexpr int kSumWmax = kSumU + 3;              // max W over T_BW rows
 constexpr int kSumVmax = kSumU + 4;              // max min(u, W) over T_BW rows (after re-binning:
                                                  // max nnz(c_i*))
-constexpr int kSumLen = kSumU + 5;
+constexpr int kSumBmax = kSumU + 5;              // max nonzero 1024-column blocks (T_BW STRUCT)
+constexpr int kSumLen = kSumU + 6;
 
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           bool hybrid_caps, Stage12Ws& ws, cudaStream_t s);

@@ -404,7 +404,7 @@ __global__ void k_validate(int64_t rows, int64_t cols, const int64_t* __restrict
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           bool hybrid_caps, Stage12Ws& ws, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 2 * sizeof(int64_t), s);
+  cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 3 * sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   if (k > 0) k_bwin<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, B.rp, B.ci, ws.bwin);
   k_stage1<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(

@@ -412,34 +412,52 @@ __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
 }
 
-// Per-warp shared-memory layout of the window class (byte offsets from the warp's base):
-//   bm   uint32[nwd]   window bitmap                           (all modes)
-//   sm   uint32[nsw]   summary bits (a bit per bm word)        (STRUCT, FILL)
-//   pre  uint16[nwd]   rank of each nonzero word's first bit    (FILL, DENSE)
-//   lst  int32[nvp]    nonzero words, ascending                 (STRUCT, FILL)
-//   vals double[nv]    the row's values in column order         (FILL, DENSE)
+// Per-warp shared-memory layout of the window class (byte offsets from the warp's base).
+// Products -> bits (COUNT, STRUCT, FILL): a bitmap over the whole window
+//   bm   uint32[nwd]   window bitmap, bit d <-> column lo + d
+//   sm   uint32[nsw]   summary, bit w <-> bm[w] != 0 (one summary word per 1024-column block)
+//   pre  uint16[nwd]   rank of each nonzero word's first bit    (FILL)
+//   lst  int32[nvp]    nonzero words, ascending                 (FILL)
+//   vals double[nv]    the row's values in column order         (FILL)
+// Sorted set -> ranks (DENSE): only the row's nonzero 1024-column blocks are materialised
+//   dir  uint16[nsw]   block -> slot + 1 (0: block empty)
+//   bits uint32[ns·32] the bitmap of each slot's block
+//   pre  uint16[ns·32] rank of each nonzero word's first bit
+//   vals double[nv]
 struct BwLayout {
-  int nwd, nsw, nvp, nv;
+  int nwd, nsw, nvp, nv, ns;
   unsigned o_sm, o_pre, o_lst, o_vals, bytes;  // per warp, bytes is a multiple of 16
 };
 
-__host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vmax) {
+__host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vmax, int64_t bmax) {
   BwLayout L;
   L.nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
   L.nsw = (L.nwd / 32 + 31) / 32 * 32;
   L.nv = (int)(vmax > 0 ? vmax : 1);
   L.nvp = (L.nv + 3) & ~3;
-  const bool summ = mode == MODE_STRUCT || mode == MODE_FILL;
-  const bool vals = mode == MODE_FILL || mode == MODE_DENSE;
-  unsigned off = 4u * L.nwd;
-  L.o_sm = off;
-  if (summ) off += 4u * L.nsw;
-  L.o_pre = off;
-  if (vals) off += 2u * L.nwd;
-  L.o_lst = off;
-  if (summ) off += 4u * L.nvp;
-  L.o_vals = off;
-  if (vals) off += 8u * L.nv;
+  L.ns = (int)(bmax > 0 ? (bmax < L.nsw ? bmax : L.nsw) : L.nsw);
+  unsigned off;
+  if (mode == MODE_DENSE) {
+    L.o_sm = 0;                                  // dir
+    off = (2u * L.nsw + 15u) & ~15u;             // bits
+    L.o_lst = off;
+    off += 128u * L.ns;
+    L.o_pre = off;
+    off += 64u * L.ns;
+    L.o_vals = off;
+    off += 8u * (L.nv + 1);  // + scratch
+  } else {
+    const bool fill = mode == MODE_FILL;
+    off = 4u * L.nwd;
+    L.o_sm = off;
+    if (mode != MODE_COUNT) off += 4u * L.nsw;
+    L.o_pre = off;
+    if (fill) off += 2u * L.nwd;
+    L.o_lst = off;
+    if (fill) off += 4u * L.nvp;
+    L.o_vals = off;
+    if (fill) off += 8u * (L.nv + 1);  // + scratch
+  }
   L.bytes = (off + 15u) & ~15u;
   return L;
 }
@@ -447,15 +465,16 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
 template <int MODE, typename IT>
 __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   constexpr bool SUMM = MODE == MODE_STRUCT || MODE == MODE_FILL;  // products -> bits + summary
-  constexpr bool VALS = MODE == MODE_FILL || MODE == MODE_DENSE;
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nwd = L.nwd, nsw = L.nsw;
   // byte addresses in the shared window
   const unsigned bm = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
   const unsigned sm = bm + L.o_sm, pre = bm + L.o_pre, lst = bm + L.o_lst, vals = bm + L.o_vals;
-  for (unsigned i = lane; i < (L.o_pre + 15u) / 16u; i += 32) sh_st_v4_zero(bm + 16u * i);  // bm (+ sm)
+  const unsigned zero_end = MODE == MODE_DENSE ? L.o_pre : L.o_pre;  // bm (+ sm) / dir + bits
+  for (unsigned i = lane; i < (zero_end + 15u) / 16u; i += 32) sh_st_v4_zero(bm + 16u * i);
   __syncwarp();
+  int bmax = 0;  // STRUCT: most nonzero 1024-column blocks in one row (sizes DENSE's slots)
 
   for (int64_t r = int64_t(blockIdx.x) * nw + w; r < a.count; r += int64_t(gridDim.x) * nw) {
     const int row = __ldg(a.perm + a.first + r);
@@ -467,15 +486,14 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       // lines 7-8 / 10 of Algorithm 1 for every product: set the column's bit.  With the
       // summary: only the lane that finds a word empty sets its summary bit, so summary
       // atomics are rare and seldom share an address.
+      // Branch-free: an idle lane (act false) re-sets the bit of column lo, a column of the row.
       walk_row<false, IT>(a, a0, a1, lane, [=](int c, double, double, bool act) {
-        if (act) {
-          const unsigned d = (unsigned)(c - lo);
-          const unsigned wa = bm + ((d >> 5) << 2);
-          if (SUMM) {
-            if (sh_atom_or(wa, 1u << (d & 31)) == 0u) sh_red_or(sm + ((d >> 10) << 2), 1u << ((d >> 5) & 31));
-          } else {
-            sh_red_or(wa, 1u << (d & 31));
-          }
+        const unsigned d = act ? (unsigned)(c - lo) : 0u;
+        const unsigned wa = bm + ((d >> 5) << 2);
+        if (SUMM) {
+          if (sh_atom_or(wa, 1u << (d & 31)) == 0u) sh_red_or(sm + ((d >> 10) << 2), 1u << ((d >> 5) & 31));
+        } else {
+          sh_red_or(wa, 1u << (d & 31));
         }
       });
       __syncwarp();
@@ -496,8 +514,40 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       __syncwarp();
       continue;
     }
+    if (MODE == MODE_STRUCT) {
+      // the sorted column set, block by nonzero block (clears bitmap and summary)
+      int32_t* oc = a.out_col + o;
+      int nb = 0;
+      for (int s0 = 0; s0 < nsw; s0 += 32) {
+        const unsigned swl = sh_ld(sm + 4u * (s0 + lane));
+        unsigned nzb = __ballot_sync(kFull, swl != 0u);
+        nb += __popc(nzb);
+        if (swl) sh_st(sm + 4u * (s0 + lane), 0u);
+        while (nzb) {
+          const int b = __ffs(nzb) - 1;
+          nzb &= nzb - 1;
+          const unsigned sw = __shfl_sync(kFull, swl, b);
+          const unsigned wa = bm + 4u * ((s0 + b) * 32 + lane);
+          unsigned word = (sw >> lane) & 1u ? sh_ld(wa) : 0u;
+          if (word) sh_st(wa, 0u);
+          const int pc = __popc(word);
+          const int inc = warp_incl_scan(pc, lane);
+          int p = nnz + inc - pc;
+          const int cb = lo + ((s0 + b) * 32 + lane) * 32;
+          while (word) {
+            oc[p++] = cb + __ffs(word) - 1;
+            word &= word - 1;
+          }
+          nnz += __shfl_sync(kFull, inc, 31);
+        }
+      }
+      bmax = max(bmax, nb);
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+      __syncwarp();
+      continue;
+    }
     int nl = 0;
-    if (SUMM) {
+    if (MODE == MODE_FILL) {
       // nonzero words in ascending order (clears the summary)
       for (int s0 = 0; s0 < nsw; s0 += 32) {
         const int s = s0 + lane;
@@ -522,7 +572,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         const int pc = __popc(word);
         const int inc = warp_incl_scan(pc, lane);
         int p = nnz + inc - pc;
-        if (VALS && q < nl) sh_st_u16(pre + 2u * wd, (unsigned)p);
+        if (q < nl) sh_st_u16(pre + 2u * wd, (unsigned)p);
         const int cb = lo + wd * 32;
         while (word) {
           oc[p++] = cb + __ffs(word) - 1;
@@ -531,43 +581,54 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         nnz += __shfl_sync(kFull, inc, 31);
       }
     }
-    if (MODE == MODE_STRUCT) {
-      for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
-      if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
-      __syncwarp();
-      continue;
-    }
-    const int32_t* sc = nullptr;
+    const unsigned dir = sm, bits = lst;  // DENSE names
+    int nslot = 0;
     if (MODE == MODE_DENSE) {
-      // the sorted column set from the symbolic pass: bits, ranks and C's columns directly
+      // the sorted column set from the symbolic pass: slots of the nonzero blocks in column
+      // order, bits, ranks, and C's columns directly
       nnz = (int)(__ldg(a.out_off + row + 1) - o);
-      sc = a.struct_col + __ldg(a.struct_off + row);
+      const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
+      int prevd = -1;  // d of the previous chunk's last column
       for (int p0 = 0; p0 < nnz; p0 += 32) {
         const int p = p0 + lane;
-        const int c = p < nnz ? __ldg(sc + p) : 0;
-        const int cprev0 = (p0 > 0 && lane == 0) ? __ldg(sc + p - 1) : 0;
-        int cprev = __shfl_up_sync(kFull, c, 1);
-        if (lane == 0) cprev = cprev0;
-        if (p < nnz) {
+        const bool in = p < nnz;
+        const int c = in ? __ldg(sc + p) : 0;
+        const int d = c - lo;
+        int dp = __shfl_up_sync(kFull, d, 1);
+        if (lane == 0) dp = prevd;
+        const bool newblk = in && (dp < 0 || (dp >> 10) != (d >> 10));
+        const unsigned nm = __ballot_sync(kFull, newblk);
+        const int slot = nslot + __popc(nm & (lanemask_lt_() | (1u << lane))) - 1;
+        if (in) {
           a.out_col[o + p] = c;
-          const unsigned d = (unsigned)(c - lo);
-          sh_red_or(bm + ((d >> 5) << 2), 1u << (d & 31));
-          if (p == 0 || (((unsigned)(cprev - lo)) >> 5) != (d >> 5)) sh_st_u16(pre + 2u * (d >> 5), (unsigned)p);
+          if (newblk) sh_st_u16(dir + 2u * (d >> 10), (unsigned)(slot + 1));
+          const unsigned wi = unsigned(slot) * 32u + ((d >> 5) & 31);
+          sh_red_or(bits + 4u * wi, 1u << (d & 31));
+          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st_u16(pre + 2u * wi, (unsigned)p);
         }
+        nslot += __popc(nm);
+        prevd = __shfl_sync(kFull, d, 31);
       }
     }
     for (int p = lane; p < nnz; p += 32) sh_st_f64(vals + 8u * p, -0.0);  // identity of +: first add == line 9
     __syncwarp();
     // lines 6, 9, 11: c_ik += a_ij b_jk at the column's rank
+    // Branch-free: an idle lane looks up column lo (present) and adds into a scratch slot.
+    // Lanes of one b_j* hold distinct columns, so no two lanes of an instruction share a slot;
+    // successive b_j* are ordered by the warp's in-order shared-memory accesses.
+    const unsigned scratch = vals + 8u * unsigned(L.nv);
     walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
-      if (act) {
-        const unsigned d = (unsigned)(c - lo);
-        const unsigned wd = d >> 5;
-        const unsigned rank = sh_ld_u16(pre + 2u * wd) + __popc(sh_ld(bm + 4u * wd) & ((1u << (d & 31)) - 1u));
-        const unsigned va = vals + 8u * rank;
-        sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
+      const unsigned d = act ? (unsigned)(c - lo) : 0u;
+      unsigned wi;
+      if (MODE == MODE_DENSE) {
+        wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
+      } else {
+        wi = d >> 5;
       }
-      __syncwarp();
+      const unsigned word = sh_ld((MODE == MODE_DENSE ? bits : bm) + 4u * wi);
+      const unsigned rank = sh_ld_u16(pre + 2u * wi) + __popc(word & ((1u << (d & 31)) - 1u));
+      const unsigned va = act ? vals + 8u * rank : scratch;
+      sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
     });
     __syncwarp();
     double* ov = a.out_val + o;
@@ -575,11 +636,14 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     if (MODE == MODE_FILL) {
       for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
     } else {
-      for (int p = lane; p < nnz; p += 32) sh_st(bm + 4u * ((unsigned)(__ldg(sc + p) - lo) >> 5), 0u);
+      for (int s = 0; s < nslot; ++s) sh_st(bits + 4u * (unsigned(s) * 32u + lane), 0u);
+      for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncwarp();
   }
+  if (MODE == MODE_STRUCT && lane == 0 && bmax > 0 && a.bw_bmax_out)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
 }
 
 }  // namespace
@@ -640,7 +704,7 @@ cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s) {
 // block chosen for the most resident warps per SM.
 template <int MODE>
 static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
-  const BwLayout L = bw_layout(MODE, a.bw_wmax, a.bw_vmax);
+  const BwLayout L = bw_layout(MODE, a.bw_wmax, a.bw_vmax, a.bw_bmax);
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
   auto kern = i32 ? k_bwrow<MODE, int> : k_bwrow<MODE, int64_t>;
   int best_nw = 1, best_warps = 0;
