@@ -567,6 +567,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.nnz_row = h->nnz_row;
     a.mode = hybrid ? MODE_FILL : ((t >= T_W64 && t <= T_W2048) || t == T_BW) ? MODE_STRUCT : MODE_COUNT;
     a.rlo = ws.rlo;
+    a.bwin = ws.bwin;
     a.bw_wmax = h->bw_wmax;
     a.bw_vmax = h->bw_vmax;
     a.bw_bmax_out = ws.summary + kSumBmax;
@@ -686,6 +687,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.struct_col = h->ctil_col;
         a.struct_off = h->ws.ctil_off;
         a.rlo = h->ws.rlo;
+        a.bwin = h->ws.bwin;
         a.bw_wmax = h->bw_wmax;
         a.bw_vmax = h->bw_vmax;
         a.bw_bmax = h->bw_bmax;

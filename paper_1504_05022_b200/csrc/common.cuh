@@ -167,7 +167,8 @@ struct Stage3Args {
   int mode;
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
-  const int32_t* rlo;         // T_BW: first column of each row's window
+  const int32_t* rlo;         // first column of each row's window (stage 1)
+  const int2* bwin;           // (first, last) column of each row of B (stage 1)
   int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
   int64_t bw_bmax;            // T_BW numeric: most nonzero 1024-column blocks in a row
   int64_t* bw_bmax_out;       // T_BW STRUCT: device max of the above (summary entry)

@@ -1,25 +1,27 @@
 // esc.cu — stage 3, classes e2048/e4096/e8192: rows whose u_i products fit one CTA's shared
 // memory but whose bound min(u_i, n) is too large for a warp table.  These are the paper's
-// group-4/5 sizes; the method here is the ESC idea of its bitonic-ESC group ([P:277-284]:
-// expand the candidates, sort, compress duplicates) with a counting sort instead of bitonic:
+// group-4/5 sizes; the method is the ESC of its bitonic-ESC group ([P:277-284]: "expand" the
+// candidates, "sort" them, "compress" duplicates), with a stable LSD radix sort of the whole
+// row in one CTA instead of the paper's bitonic sort:
 //
-//   1. expand: every product (c, a_ij·b_jk, p) with p its position in the row's product order
-//      (j ascending, then k ascending: the order of Algorithm 1 [P:121-135]);
-//   2. counting sort into NB ≈ u buckets by the monotone bucket b(c) = ⌊(c-lo)·NB/W⌋
-//      (count, exclusive scan, scatter — shared-memory integer atomics only);
-//   3. each bucket (a few entries) sorted by (c, p) with an insertion sort;
-//   4. compress: equal columns fused in p order — the oracle's accumulation order, so values
-//      are bit-identical to it (R1) — then an ordered write of the buckets.
-// No hash probing, no value atomics; cost O(u) plus the small per-bucket sorts.
+//   1. expand: every product (c - lo, a_ij·b_jk) lands at its position p in the row's
+//      product order (j ascending, then k ascending: Algorithm 1 [P:121-135]); p comes from a
+//      block scan of nnz(b_j*) — no atomics, one warp per a_ij, coalesced b_j* loads;
+//   2. sort: cub::BlockRadixSort (stable) over the bits of the row's column window, items in
+//      blocked p order, so equal columns stay in p order;
+//   3. compress: each run of equal columns is summed left to right (the oracle's order, so
+//      values are bit-identical to it, R1) and the row is written in order.
+// COUNT (precise symbolic) uses the CTA hash of the same size (stage3.cu): counting needs no order.
 #include <climits>
+#include <type_traits>
+
+#include <cub/block/block_radix_sort.cuh>
 
 #include "common.cuh"
 
 namespace sg {
 
 namespace {
-
-constexpr int kEscChunk = 128;  // products per work item
 
 template <int NT>
 __device__ __forceinline__ int esc_block_excl_scan(int v, int* total, int* s_w) {
@@ -50,245 +52,171 @@ __device__ __forceinline__ int esc_block_excl_scan(int v, int* total, int* s_w) 
   return ex;
 }
 
-template <int NT>
-struct EscBatch {
-  long long bs[NT];
-  int len[NT];
-  int pex[NT];   // exclusive product prefix within the batch
-  int cinc[NT];  // inclusive prefix of work items
-  double av[NT];
+constexpr int kEscRadixBits = 6;  // digit width of the block radix sort (4 passes for 23-bit windows)
+
+template <int NT, int IPT, bool VALS>
+struct EscSmem {
+  static constexpr int U = NT * IPT;
+  using Sort = cub::BlockRadixSort<unsigned, NT, IPT, typename std::conditional<VALS, double, cub::NullType>::type,
+                                   kEscRadixBits>;
+  struct Rows {
+    unsigned key[U];
+    double val[VALS ? U : 1];
+  };
+  union {
+    typename Sort::TempStorage sort;
+    Rows rows;
+  };
 };
 
-// Visit every product of row [a0, a1) as f(q, a_ij, p): balanced work items of kEscChunk
-// products, p = the product's index in the row's (j, k) order.
-template <int NT, bool VALS, typename F>
-__device__ __forceinline__ void esc_products(const Stage3Args& a, int64_t a0, int64_t a1, EscBatch<NT>& sb,
-                                             int* s_w, F&& f) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = NT / 32;
-  int pbase = 0;
-  for (int64_t e0 = a0; e0 < a1; e0 += NT) {
-    const int64_t e = e0 + threadIdx.x;
-    int len = 0;
-    if (e < a1) {
-      const int j = __ldg(a.A.ci + e);
-      const int64_t bs = __ldg(a.B.rp + j);
-      len = (int)(__ldg(a.B.rp + j + 1) - bs);
-      sb.bs[threadIdx.x] = bs;
-      sb.len[threadIdx.x] = len;
-      if (VALS) sb.av[threadIdx.x] = __ldg(a.A.val + e);
-    }
-    int ptot;
-    const int pex = esc_block_excl_scan<NT>(len, &ptot, s_w);
-    const int nch = (len + kEscChunk - 1) / kEscChunk;
-    int ctot;
-    const int cex = esc_block_excl_scan<NT>(nch, &ctot, s_w);
-    sb.pex[threadIdx.x] = pex;
-    sb.cinc[threadIdx.x] = cex + nch;
-    __syncthreads();
-    for (int item = w; item < ctot; item += NW) {
-      int lo = 0, hi = NT - 1;  // first t with cinc[t] > item
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sb.cinc[mid] > item) hi = mid;
-        else lo = mid + 1;
-      }
-      const int t = lo;
-      const int first = sb.cinc[t] - (sb.len[t] + kEscChunk - 1) / kEscChunk;
-      const int off0 = (item - first) * kEscChunk;
-      const int off1 = min(off0 + kEscChunk, sb.len[t]);
-      const double at = VALS ? sb.av[t] : 0.0;
-      const int pt = pbase + sb.pex[t];
-      for (int off = off0 + lane; off < off1; off += 32) f((int64_t)sb.bs[t] + off, at, pt + off);
-    }
-    pbase += ptot;
-    __syncthreads();
-  }
-}
-
-template <int LOG2U, int NT>
-__global__ void __launch_bounds__(NT, 1) k_cta_esc(Stage3Args a) {
-  constexpr int UMAX = 1 << LOG2U;
-  constexpr int NBMAX = UMAX;  // ~1 product per bucket: the per-bucket sorts are trivial
+template <int NT, int IPT, int MODE, typename IT>
+__global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
+  constexpr bool VALS = MODE == MODE_FILL;
+  constexpr int U = NT * IPT;
   constexpr int NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const bool fill = a.mode == MODE_FILL;
-  // layout: vals double[UMAX] (fill) | keys int[UMAX] | pidx int[UMAX] (fill) | bstart int[NBMAX+1] | bcur int[NBMAX]
-  double* vals = reinterpret_cast<double*>(smem);
-  int* keys = reinterpret_cast<int*>(smem + (fill ? size_t(UMAX) * sizeof(double) : 0));
-  int* pidx = keys + UMAX;
-  int* bstart = keys + (fill ? 2 * UMAX : UMAX);
-  int* bcur = bstart + NBMAX + 1;
-  __shared__ EscBatch<NT> sb;
+  using SM = EscSmem<NT, IPT, VALS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  __shared__ IT s_bs[NT];
+  __shared__ int s_len[NT], s_pex[NT];
+  __shared__ double s_av[VALS ? NT : 1];
   __shared__ int s_w[NW + 1];
-  __shared__ int s_red[3 * NW];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ unsigned s_max[NW];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
   for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
     const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    // window [lo, hi] and u of the row
-    int lo = INT_MAX, hi = -1, u = 0;
-    for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
-      const int j = __ldg(a.A.ci + e);
-      const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
-      if (be > bs) {
-        lo = min(lo, __ldg(a.B.ci + bs));
-        hi = max(hi, __ldg(a.B.ci + be - 1));
-        u += (int)(be - bs);
+    // 1. expand (lines 3-6 of Algorithm 1): product p of the row at rows.key/val[p]
+    int u = 0;
+    unsigned kmax = 0;
+    for (int64_t e0 = a0; e0 < a1; e0 += NT) {
+      const int64_t e = e0 + tid;
+      int len = 0;
+      if (e < a1) {
+        const int j = __ldg(a.A.ci + e);
+        const int64_t b0 = __ldg(a.B.rp + j);
+        len = (int)(__ldg(a.B.rp + j + 1) - b0);
+        s_bs[tid] = (IT)b0;
+        if (VALS) s_av[tid] = __ldg(a.A.val + e);
       }
+      int tot;
+      const int ex = esc_block_excl_scan<NT>(len, &tot, s_w);  // syncs
+      s_len[tid] = len;
+      s_pex[tid] = u + ex;
+      __syncthreads();
+      const int na = (int)((a1 - e0) < NT ? (a1 - e0) : NT);
+      for (int t = w; t < na; t += NW) {
+        const IT bs = s_bs[t];
+        const int lt = s_len[t], pe = s_pex[t];
+        const double at = VALS ? s_av[t] : 0.0;
+        for (int q = lane; q < lt; q += 32) {
+          const unsigned k = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
+          sm.rows.key[pe + q] = k;
+          kmax = k > kmax ? k : kmax;
+          if (VALS) sm.rows.val[pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
+        }
+      }
+      u += tot;
+      __syncthreads();
     }
+    // window bits of the row (the radix sort's end bit)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      u += __shfl_xor_sync(0xffffffffu, u, o);
+      const unsigned x = __shfl_xor_sync(0xffffffffu, kmax, o);
+      kmax = x > kmax ? x : kmax;
     }
-    if (lane == 0) {
-      s_red[w] = lo;
-      s_red[NW + w] = hi;
-      s_red[2 * NW + w] = u;
+    if (lane == 0) s_max[w] = kmax;
+    // 2. sort: blocked items in p order; padding sorts last (stable: after equal keys)
+    unsigned k[IPT];
+    typename std::conditional<VALS, double, cub::NullType>::type v[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int p = tid * IPT + i;
+      k[i] = p < u ? sm.rows.key[p] : 0xffffffffu;
+      if constexpr (VALS) v[i] = p < u ? sm.rows.val[p] : 0.0;
     }
     __syncthreads();
-    lo = INT_MAX;
-    hi = -1;
-    u = 0;
-    for (int k = 0; k < NW; ++k) {
-      lo = min(lo, s_red[k]);
-      hi = max(hi, s_red[NW + k]);
-      u += s_red[2 * NW + k];
+    unsigned km = 0;
+#pragma unroll
+    for (int x = 0; x < NW; ++x) km = s_max[x] > km ? s_max[x] : km;
+    const int end_bit = km ? 32 - __clz(km) : 1;
+    if constexpr (VALS) {
+      typename SM::Sort(sm.sort).Sort(k, v, 0, end_bit);
+    } else {
+      typename SM::Sort(sm.sort).Sort(k, 0, end_bit);
     }
-    int NB = 32;
-    while (NB < NBMAX && NB < u) NB <<= 1;
-    const float scale = (float)NB / (float)(int64_t(hi) - lo + 1);
-    for (int b = threadIdx.x; b <= NB; b += NT) bstart[b] = 0;
     __syncthreads();
-    // 1-2. expand + count per bucket
-    esc_products<NT, false>(a, a0, a1, sb, s_w, [&](int64_t q, double, int) {
-      const int c = __ldg(a.B.ci + q);
-      const int b = min((int)__fmul_rz((float)(c - lo), scale), NB - 1);  // monotone in c
-      atomicAdd(&bstart[b], 1);
-    });
-    // exclusive scan of the bucket counts (each thread owns NB/NT or 1 buckets)
-    {
-      constexpr int PER = NBMAX / NT > 0 ? NBMAX / NT : 1;
-      const int b0 = threadIdx.x * PER;
-      int v[PER];
-      int loc = 0;
+    const unsigned pad = end_bit >= 32 ? 0xffffffffu : ((1u << end_bit) - 1u);
+    (void)pad;
 #pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        v[k] = (b0 + k < NB) ? bstart[b0 + k] : 0;
-        loc += v[k];
-      }
-      int tot;
-      int run = esc_block_excl_scan<NT>(loc, &tot, s_w);
+    for (int i = 0; i < IPT; ++i) {
+      sm.rows.key[tid * IPT + i] = k[i];
+      if constexpr (VALS) sm.rows.val[tid * IPT + i] = v[i];
+    }
+    __syncthreads();
+    // 3. compress: heads of runs of equal columns; run sums left to right (lines 9, 11)
+    int heads = 0;
 #pragma unroll
-      for (int k = 0; k < PER; ++k)
-        if (b0 + k < NB) {
-          bstart[b0 + k] = run;
-          bcur[b0 + k] = run;
-          run += v[k];
+    for (int i = 0; i < IPT; ++i) {
+      const int p = tid * IPT + i;
+      const bool head = p < u && (p == 0 || sm.rows.key[p - 1] != k[i]);
+      if (head) {
+        ++heads;
+        if constexpr (VALS) {
+          double acc = v[i];
+          for (int x = p + 1; x < u && sm.rows.key[x] == k[i]; ++x) acc = __dadd_rn(acc, sm.rows.val[x]);
+          v[i] = acc;
         }
-      if (threadIdx.x == 0) bstart[NB] = tot;
+      } else {
+        k[i] = 0xffffffffu;  // not a head
+      }
+    }
+    int nnz;
+    int pos = esc_block_excl_scan<NT>(heads, &nnz, s_w);  // syncs: all reads above are done
+    if (MODE == MODE_FILL) {
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        if (tid * IPT + i < u && k[i] != 0xffffffffu) {
+          sm.rows.key[pos] = k[i];
+          if constexpr (VALS) sm.rows.val[pos] = v[i];
+          ++pos;
+        }
+      }
       __syncthreads();
+      const int64_t o = __ldg(a.out_off + row);
+      for (int i = tid; i < nnz; i += NT) {
+        a.out_col[o + i] = (int)sm.rows.key[i] + lo;
+        if constexpr (VALS) a.out_val[o + i] = sm.rows.val[i];
+      }
     }
-    // 2. scatter (column, product index, value) into the buckets
-    esc_products<NT, true>(a, a0, a1, sb, s_w, [&](int64_t q, double at, int p) {
-      const int c = __ldg(a.B.ci + q);
-      const int b = min((int)__fmul_rz((float)(c - lo), scale), NB - 1);
-      const int slot = atomicAdd(&bcur[b], 1);
-      keys[slot] = c;
-      if (fill) {
-        pidx[slot] = p;
-        vals[slot] = __dmul_rn(at, __ldg(a.B.val + q));  // line 6: value <- a_ij b_jk
-      }
-    });
-    // 3-4. sort each bucket by (column, p), fuse equal columns in p order
-    for (int b = threadIdx.x; b < NB; b += NT) {
-      const int s0 = bstart[b], s1 = bstart[b + 1];
-      for (int x = s0 + 1; x < s1; ++x) {
-        const int kx = keys[x];
-        const int px = fill ? pidx[x] : 0;
-        const double vx = fill ? vals[x] : 0.0;
-        int y = x - 1;
-        while (y >= s0 && (keys[y] > kx || (fill && keys[y] == kx && pidx[y] > px))) {
-          keys[y + 1] = keys[y];
-          if (fill) {
-            pidx[y + 1] = pidx[y];
-            vals[y + 1] = vals[y];
-          }
-          --y;
-        }
-        keys[y + 1] = kx;
-        if (fill) {
-          pidx[y + 1] = px;
-          vals[y + 1] = vx;
-        }
-      }
-      int d = s0;  // fused entries are written to the front of the bucket
-      for (int x = s0; x < s1; ++x) {
-        if (x > s0 && keys[x] == keys[d - 1]) {
-          if (fill) vals[d - 1] = __dadd_rn(vals[d - 1], vals[x]);  // line 11: accumulate
-        } else {
-          keys[d] = keys[x];
-          if (fill) vals[d] = vals[x];  // line 9: c_ik <- value
-          ++d;
-        }
-      }
-      bcur[b] = d - s0;  // distinct columns of the bucket
-    }
+    if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncthreads();
-    // 5. ordered write: exclusive scan of the distinct counts
-    {
-      constexpr int PER = NBMAX / NT > 0 ? NBMAX / NT : 1;
-      const int b0 = threadIdx.x * PER;
-      int loc = 0;
-#pragma unroll
-      for (int k = 0; k < PER; ++k)
-        if (b0 + k < NB) loc += bcur[b0 + k];
-      int tot;
-      int pos = esc_block_excl_scan<NT>(loc, &tot, s_w);
-      if (fill) {
-        const int64_t o = __ldg(a.out_off + row);
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int b = b0 + k;
-          if (b >= NB) break;
-          const int s0 = bstart[b];
-          for (int t = 0; t < bcur[b]; ++t) {
-            a.out_col[o + pos + t] = keys[s0 + t];
-            a.out_val[o + pos + t] = vals[s0 + t];
-          }
-          pos += bcur[b];
-        }
-      }
-      if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = tot;
-      __syncthreads();
-    }
   }
 }
 
-int esc_sms() {
-  int dev = 0, n = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
-}
-
-template <int LOG2U, int NT>
-cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
-  constexpr int UMAX = 1 << LOG2U;
-  const bool fill = a.mode == MODE_FILL;
-  const size_t sm = size_t(UMAX) * (fill ? 16 : 4) + size_t(UMAX) * 8 + 8;
-  auto kern = k_cta_esc<LOG2U, NT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <int NT, int IPT, int MODE, typename IT>
+cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
+  using SM = EscSmem<NT, IPT, MODE == MODE_FILL>;
+  const size_t bytes = sizeof(SM);
+  auto kern = k_esc_sort<NT, IPT, MODE, IT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
+  if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  int64_t grid = int64_t(esc_sms()) * per_sm * 4;
+  int64_t grid = int64_t(num_sms()) * per_sm;
   if (grid > a.count) grid = a.count;
-  kern<<<(unsigned)grid, NT, sm, s>>>(a);
+  kern<<<(unsigned)grid, NT, bytes, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int NT, int IPT>
+cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
+  const bool i32 = a.b_nnz < (int64_t(1) << 31);
+  return i32 ? launch_esc_k<NT, IPT, MODE_FILL, int>(a, s) : launch_esc_k<NT, IPT, MODE_FILL, int64_t>(a, s);
 }
 
 }  // namespace
@@ -296,9 +224,9 @@ cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   switch (tier) {
-    case T_E2048: return launch_esc_t<11, 256>(a, s);
-    case T_E4096: return launch_esc_t<12, 256>(a, s);
-    case T_E8192: return launch_esc_t<13, 512>(a, s);
+    case T_E2048: return launch_esc_t<256, 8>(a, s);
+    case T_E4096: return launch_esc_t<256, 16>(a, s);
+    case T_E8192: return launch_esc_t<512, 16>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }

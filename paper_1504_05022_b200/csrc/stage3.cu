@@ -455,7 +455,7 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
       return launch_warp_tier(tier, a, s);
     case T_BW:
       return launch_bw_tier(a, s);
-    // bucket ESC for values; counting only needs distinct keys: the CTA hash of the same size
+    // ESC (sorted) for values; counting only needs distinct keys: the CTA hash of the same size
     case T_E2048:
       if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * 4, a.count, 1, a, s);
       return launch_esc(tier, a, s);
