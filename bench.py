@@ -339,17 +339,17 @@ def run_gpu(args):
         if not hybrid:
             sym_ms = st0["stage_ms"][1]
             alg = 28 * m0 + 4 * dA0.nnz + 4 * min(Bm0.nnz, st0["sum_u"]) + 4 * nnz0
-            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bwrow COUNT / k_wrow STRUCT / counts)" % name0,
+            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bwrow STRUCT / k_wrow, k_cta_hash COUNT)" % name0,
                           "symbolic"))
         for cls_name, c in st0["classes"].items():
             if c["ms"] <= 0:
                 continue
-            dense = (not hybrid) and cls_name.startswith("w")
+            dense = (not hybrid) and cls_name == "bw"
             alg = (36 if dense else 28) * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + \
                 12 * c["c_entries"] + (4 * c["c_entries"] if dense else 0)
             kname = "k_bwrow" if cls_name == "bw" else \
-                ("k_wdense" if dense else "k_wrow") if cls_name.startswith("w") else \
-                "k_group" if cls_name.startswith("g") else "k_cta_esc" if cls_name.startswith("e") else \
+                "k_esc_sort" if cls_name.startswith("w") else \
+                "k_group" if cls_name.startswith("g") else "k_esc_sort" if cls_name.startswith("e") else \
                 "k_cta_hash" if cls_name.startswith("c") else ("k_long" if hybrid else "k_long_bm_fill")
             cands.append((c["ms"], alg, "%s: stage-3 class %s (%s)" % (name0, cls_name, kname), cls_name))
     best = max(cands, key=lambda x: x[0])

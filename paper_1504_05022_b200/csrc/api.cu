@@ -543,7 +543,6 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   {
     // precise: C~ holds only the warp classes' sorted column sets (STRUCT)
     bool need = hybrid;
-    for (int t = T_W64; t <= T_W2048; ++t) need = need || h->tier_count[t] > 0;
     need = need || h->tier_count[T_BW] > 0;
     AL(h, &h->ctil_col, need ? h->sum_cap : 1);
   }
@@ -565,7 +564,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.out_col = h->ctil_col;
     a.out_val = h->ctil_val;
     a.nnz_row = h->nnz_row;
-    a.mode = hybrid ? MODE_FILL : ((t >= T_W64 && t <= T_W2048) || t == T_BW) ? MODE_STRUCT : MODE_COUNT;
+    a.mode = hybrid ? MODE_FILL : (t == T_BW) ? MODE_STRUCT : MODE_COUNT;
     a.rlo = ws.rlo;
     a.bwin = ws.bwin;
     a.bw_wmax = h->bw_wmax;
@@ -682,7 +681,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.out_col = c_col_idx;
         a.out_val = c_val;
         a.nnz_row = nullptr;
-        const bool dense = (t >= T_W64 && t <= T_W2048) || t == T_BW;
+        const bool dense = t == T_BW;
         a.mode = dense ? MODE_DENSE : MODE_FILL;
         a.struct_col = h->ctil_col;
         a.struct_off = h->ws.ctil_off;

@@ -102,7 +102,7 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
   if (t == T_EMPTY) return u == 0;
   if (t == T_BW) return 0;  // only rows that were window rows in the symbolic pass (below)
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
-  if (t >= T_W64 && t <= T_W2048) return (int64_t(64) << (t - T_W64)) >= 2 * nnz;  // dense: S >= 2·nnz
+  if (t >= T_W64 && t <= T_W2048) return (int64_t(64) << (t - T_W64)) >= 2 * nnz && u <= (int64_t(64) << (t - T_W64));  // S >= 2·nnz, u <= S (ESC items)
   if (t >= T_C2048 && t <= T_C8192) return nnz <= (int64_t(2048) << (t - T_C2048));
   if (t >= T_E2048 && t <= T_E8192) return u <= (int64_t(2048) << (t - T_E2048));
   return 1;
@@ -113,6 +113,8 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
 __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_class, TierParams p) {
   if (u == 0) return T_EMPTY;
   if (sym_class == T_BW) return T_BW;  // window and bound unchanged: nnz <= min(u, W) <= kBwMaxV
+  // warp classes: the numeric pass sorts the row's u <= 0.8·S products in one CTA (ESC)
+  if (p.force_tier < 0 && sym_class >= T_W64 && sym_class <= T_W2048) return sym_class;
   const bool has_struct = sym_class >= T_W64 && sym_class <= T_W2048;
   if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz) &&
       (has_struct || p.force_tier < T_W64 || p.force_tier > T_W2048) &&
@@ -219,6 +221,8 @@ cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s);
 int num_sms();
 // bucket-ESC classes (esc.cu)
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s);
+// the same sort for the warp classes' rows in FILL mode: one CTA of S items per row
+cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s);
 // PRECISE long rows: bitmap over the column window (COUNT: nnz; FILL: ranks → C)
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s);
 

@@ -221,6 +221,20 @@ cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
 
 }  // namespace
 
+// Rows of the warp classes (u <= 0.8·S) sorted in one CTA of S items.
+cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  switch (S) {
+    case 64: return launch_esc_t<32, 2>(a, s);
+    case 128: return launch_esc_t<32, 4>(a, s);
+    case 256: return launch_esc_t<64, 4>(a, s);
+    case 512: return launch_esc_t<64, 8>(a, s);
+    case 1024: return launch_esc_t<128, 8>(a, s);
+    case 2048: return launch_esc_t<256, 8>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   switch (tier) {

@@ -20,10 +20,9 @@ namespace sg {
 namespace {
 
 constexpr int kBmNT = 512;
-constexpr int kTileWords = 8192;                  // 256 Ki columns per tile (64 KB with prefix)
+constexpr int kTileWords = 32768;                 // 1 Mi columns per tile (192 KB with prefix)
 constexpr int kChunk = 256;                       // products per work item (load balance)
 constexpr int64_t kTileBits = int64_t(kTileWords) * 32;
-constexpr size_t kBmSmem = size_t(kTileWords) * 6;  // bitmap + one prefix per word pair
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
@@ -147,15 +146,21 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
     int lo, hi;
     row_window(a, a0, a1, s_red, lo, hi);
     if (threadIdx.x == 0) s_cnt = 0;
-    for (int64_t base = lo; base <= hi; base += kTileBits) {
-      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
+    // tile: the row's window, at most kTileBits columns, in multiples of kBmNT words
+    const int64_t wwords = (int64_t(hi) - lo) / 32 + 1;
+    const int64_t tmax = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
+                             ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
+    const int tw = (int)((wwords < tmax ? wwords : tmax) + kBmNT - 1) / kBmNT * kBmNT;
+    const int64_t tbits = int64_t(tw) * 32;
+    for (int64_t base = lo; base <= hi; base += tbits) {
+      for (int k = threadIdx.x; k < tw; k += kBmNT) bm[k] = 0u;
       __syncthreads();
       for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
         const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+        if (d >= 0 && d < tbits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
       });
       unsigned c = 0;
-      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) c += __popc(bm[k]);
+      for (int k = threadIdx.x; k < tw; k += kBmNT) c += __popc(bm[k]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, (unsigned long long)c);
@@ -169,32 +174,37 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
 __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
-  int* pre = reinterpret_cast<int*>(smem + size_t(kTileWords) * sizeof(unsigned));
+  const int64_t tmax0 = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
+                            ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
+  int* pre = reinterpret_cast<int*>(smem + size_t(tmax0) * sizeof(unsigned));
   __shared__ int s_red[2 * (kBmNT / 32)];
   __shared__ int s_w[kBmNT / 32 + 1];
   __shared__ BmBatch sb;
-  constexpr int WPT = kTileWords / kBmNT;  // words per thread in the prefix scan
   for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     const int64_t o = __ldg(a.out_off + row);
     int lo, hi;
     row_window(a, a0, a1, s_red, lo, hi);
+    const int64_t wwords = (int64_t(hi) - lo) / 32 + 1;
+    const int64_t tmax = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
+                             ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
+    const int tw = (int)((wwords < tmax ? wwords : tmax) + kBmNT - 1) / kBmNT * kBmNT;
+    const int64_t tbits = int64_t(tw) * 32;
+    const int WPT = tw / kBmNT;  // words per thread in the prefix scan
     int64_t done = 0;  // entries of the row already placed by earlier tiles
-    for (int64_t base = lo; base <= hi; base += kTileBits) {
-      for (int k = threadIdx.x; k < kTileWords; k += kBmNT) bm[k] = 0u;
+    for (int64_t base = lo; base <= hi; base += tbits) {
+      for (int k = threadIdx.x; k < tw; k += kBmNT) bm[k] = 0u;
       __syncthreads();
       for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
         const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < kTileBits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
+        if (d >= 0 && d < tbits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
       });
       // exclusive prefix popcount over the tile's words (thread t owns words [t·WPT, +WPT))
       int loc = 0;
-#pragma unroll 4
       for (int k = 0; k < WPT; ++k) loc += __popc(bm[threadIdx.x * WPT + k]);
       int tot;
       int run = block_excl_scan_i<kBmNT>(loc, &tot, s_w);
-#pragma unroll 4
       for (int k = 0; k < WPT; ++k) {
         const int wi = threadIdx.x * WPT + k;
         const unsigned bits = bm[wi];
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
       // values: every product of a column in this tile adds into its rank (line 11)
       for_each_product<true>(a, a0, a1, sb, s_w, [&](int64_t q, double at) {
         const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < kTileBits) {
+        if (d >= 0 && d < tbits) {
           const int wi = (int)(d >> 5);
           const unsigned below = (1u << (d & 31)) - 1u;
           const int rank = pre[wi >> 1] + ((wi & 1) ? __popc(bm[wi - 1]) : 0) + __popc(bm[wi] & below);
@@ -242,7 +252,10 @@ int sm_count() {
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const bool fill = a.mode == MODE_FILL;
-  const size_t sm = fill ? kBmSmem : size_t(kTileWords) * sizeof(unsigned);
+  // tiles never exceed the column range [0, n): size shared memory by it (c3b: 8 Ki words)
+  const int64_t nwords = ((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT;
+  const int64_t tw = nwords < kTileWords ? nwords : kTileWords;
+  const size_t sm = size_t(tw) * (fill ? 6 : 4);
   auto kern = fill ? k_long_bm_fill : k_long_bm_count;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

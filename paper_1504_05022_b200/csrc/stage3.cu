@@ -452,6 +452,9 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_W512:
     case T_W1024:
     case T_W2048:
+      // values: the row's products sorted in one CTA (ESC, esc.cu) — cheaper than hash + sort;
+      // counting / structure / dense lookup: the warp hash (warp.cu)
+      if (a.mode == MODE_FILL) return launch_esc_items(64 << (tier - T_W64), a, s);
       return launch_warp_tier(tier, a, s);
     case T_BW:
       return launch_bw_tier(a, s);
