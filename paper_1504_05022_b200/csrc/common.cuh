@@ -174,6 +174,9 @@ struct Stage3Args {
   int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
   int64_t bw_bmax;            // T_BW numeric: most nonzero 1024-column blocks in a row
   int64_t* bw_bmax_out;       // T_BW STRUCT: device max of the above (summary entry)
+  int32_t* bw_ovf_list;       // T_BW STRUCT: rows with more nonzero blocks than the slots
+  int32_t* bw_ovf_cnt;        //   (re-run over the full-window bitmap; device counter)
+  const int32_t* count_dev;   // if set, the kernel reads its row count here (rows = perm[0..))
 };
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------

@@ -18,6 +18,7 @@
 //   MODE_DENSE   precise numeric: look columns up in a read-only key -> position table built
 //                from the STRUCT set; accumulate into a dense array already in column order.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -476,7 +477,8 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   __syncwarp();
   int bmax = 0;  // STRUCT: most nonzero 1024-column blocks in one row (sizes DENSE's slots)
 
-  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < a.count; r += int64_t(gridDim.x) * nw) {
+  const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;
+  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < count; r += int64_t(gridDim.x) * nw) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
@@ -646,6 +648,108 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
 }
 
+
+// ----------------------------------------------------------------------------------------
+// T_BW STRUCT with a block directory: only the row's nonzero 1024-column blocks get a
+// bitmap slot (allocated on first touch, warp-synchronously: the lanes of one b_j* hold
+// ascending columns, so each newly touched block is claimed by the first lane of its run).
+// Per warp: dir uint16[nsw] (block -> slot + 1) | bits uint32[ns·32].  ~2.3 KB per warp
+// instead of W/8: 2x the resident warps on c2.  Inserting is a fire-and-forget shared OR.  A row touching more than ns blocks is appended to an overflow list and redone by the
+// full-window kernel.
+struct Bs2Layout {
+  int nsw, ns;
+  unsigned o_bits, o_wmask, bytes;
+};
+
+__host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns) {
+  Bs2Layout L;
+  const int nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
+  L.nsw = (nwd / 32 + 31) / 32 * 32;
+  L.ns = ns;
+  L.o_bits = (2u * L.nsw + 15u) & ~15u;
+  L.o_wmask = L.o_bits + 128u * ns;
+  L.bytes = L.o_wmask;
+  return L;
+}
+
+template <typename IT>
+__global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
+  extern __shared__ __align__(16) uint32_t s_bw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
+  const unsigned bits = dir + L.o_bits;
+  const int ns = L.ns, nsw = L.nsw;
+  for (unsigned i = lane; i < L.bytes / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
+  __syncwarp();
+  const unsigned lt = lanemask_lt_();
+  int bmax = 0;
+
+  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < a.count; r += int64_t(gridDim.x) * nw) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int nslot = 0;  // warp-uniform
+    walk_row<false, IT>(a, a0, a1, lane, [=, &nslot](int c, double, double, bool act) {
+      const unsigned d = act ? (unsigned)(c - lo) : 0u;
+      const unsigned blk = d >> 10;
+      unsigned s = act ? sh_ld_u16(dir + 2u * blk) : 1u;
+      const bool need = s == 0u;
+      const unsigned nm = __ballot_sync(kFull, need);
+      if (nm) {  // first touch of some blocks: the first lane of each block's run claims a slot
+        const unsigned bp = __shfl_up_sync(kFull, blk, 1);
+        const bool lead = need && (lane == 0 || !((nm >> (lane - 1)) & 1u) || bp != blk);
+        const unsigned lm = __ballot_sync(kFull, lead);
+        const int id = nslot + __popc(lm & lt) + 1;
+        if (lead && id <= ns) sh_st_u16(dir + 2u * blk, (unsigned)id);
+        nslot += __popc(lm);
+        __syncwarp();
+        if (need) s = sh_ld_u16(dir + 2u * blk);
+      }
+      if (act && s != 0u) sh_red_or(bits + 4u * ((s - 1u) * 32u + ((d >> 5) & 31u)), 1u << (d & 31));
+    });
+    __syncwarp();
+    if (nslot > ns) {
+      // too many blocks: clear and hand the row to the full-window kernel
+      for (int s = 0; s < ns; ++s) sh_st(bits + 4u * (unsigned(s) * 32u + lane), 0u);
+      for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
+      if (lane == 0) a.bw_ovf_list[atomicAdd(a.bw_ovf_cnt, 1)] = row;
+      __syncwarp();
+      continue;
+    }
+    // the sorted column set: blocks in ascending order, words by their wmask bits
+    const int64_t o = __ldg(a.out_off + row);
+    int32_t* oc = a.out_col + o;
+    int nnz = 0;
+    for (int s0 = 0; s0 < nsw; s0 += 32) {
+      const unsigned dl = sh_ld_u16(dir + 2u * (s0 + lane));
+      unsigned nzb = __ballot_sync(kFull, dl != 0u);
+      if (dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
+      while (nzb) {
+        const int b = __ffs(nzb) - 1;
+        nzb &= nzb - 1;
+        const unsigned slot = __shfl_sync(kFull, dl, b) - 1u;
+        const unsigned wa = bits + 4u * (slot * 32u + lane);
+        unsigned word = sh_ld(wa);
+        if (word) sh_st(wa, 0u);
+        const int pc = __popc(word);
+        const int inc = warp_incl_scan(pc, lane);
+        int p = nnz + inc - pc;
+        const int cb = lo + ((s0 + b) * 32 + lane) * 32;
+        while (word) {
+          oc[p++] = cb + __ffs(word) - 1;
+          word &= word - 1;
+        }
+        nnz += __shfl_sync(kFull, inc, 31);
+      }
+    }
+    bmax = max(bmax, nslot);
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncwarp();
+  }
+  if (lane == 0 && bmax > 0 && a.bw_bmax_out)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
+}
+
 }  // namespace
 
 template <typename K>
@@ -732,8 +836,44 @@ static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+constexpr int kBs2Slots = 16;
+
+template <typename IT>
+static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
+  const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots);
+  auto kern = k_bw_struct2<IT>;
+  constexpr int nw = 8;
+  const size_t bytes = size_t(nw) * L.bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.count + nw - 1) / nw;
+  const int64_t cap = int64_t(num_sms()) * per_sm;
+  kern<<<(unsigned)(need < cap ? need : cap), nw * 32, bytes, s>>>(a, L);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
+  const int64_t blocks = (a.bw_wmax + 1023) / 1024;
+  static const bool no_bs2 = getenv("SPGEMM_NO_BS2") != nullptr;  // A/B switch (development)
+  if (a.mode == MODE_STRUCT && blocks > kBs2Slots && a.bw_ovf_list && a.bw_ovf_cnt && !no_bs2) {
+    // block-directory pass, then the full-window pass over the rows that overflowed it
+    cudaError_t e = cudaMemsetAsync(a.bw_ovf_cnt, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    const bool i32 = a.b_nnz < (int64_t(1) << 31);
+    e = i32 ? launch_bs2<int>(a, s) : launch_bs2<int64_t>(a, s);
+    if (e != cudaSuccess) return e;
+    Stage3Args b = a;
+    b.perm = a.bw_ovf_list;
+    b.first = 0;
+    b.count = a.count;  // grid bound; the kernel reads the real count from count_dev
+    b.count_dev = a.bw_ovf_cnt;
+    return launch_bw_mode<MODE_STRUCT>(b, s);
+  }
   switch (a.mode) {
     case MODE_FILL: return launch_bw_mode<MODE_FILL>(a, s);
     case MODE_STRUCT: return launch_bw_mode<MODE_STRUCT>(a, s);
