@@ -12,6 +12,8 @@
 //   3. compress: each run of equal columns is summed left to right (the oracle's order, so
 //      values are bit-identical to it, R1) and the row is written in order.
 // COUNT (precise symbolic) uses the CTA hash of the same size (stage3.cu): counting needs no order.
+// The warp classes' rows (u <= 2048) are sorted by a run merge instead (k_esc_merge below):
+// every b_j* is already sorted, so ⌈log2 runs⌉ stable pairwise merges sort the row.
 #include <climits>
 #include <type_traits>
 
@@ -213,24 +215,207 @@ cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------------------
+// Run-merge ESC.  Every b_j* is sorted (Q3), so the expanded row is already a sequence of
+// sorted runs (one per nonempty b_j*, in j order).  Merging runs pairwise, left run first on
+// ties (stable: product order p is kept among equal columns), sorts the row in ⌈log2 runs⌉
+// rounds instead of one radix pass per digit.  Each round: thread t produces output positions
+// [t·IPT, (t+1)·IPT): binary search for its pair of runs and its merge-path split, then a
+// sequential merge; keys and values ping-pong between two shared buffers.
+template <int NT, int IPT>
+struct MergeSmem {
+  static constexpr int U = NT * IPT;
+  unsigned key[2][U];
+  double val[2][U];
+  unsigned short rb[U + 2];  // run boundaries (nonempty runs)
+};
+
+template <int NT, int IPT, typename IT>
+__global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
+  constexpr int U = NT * IPT;
+  constexpr int NW = NT / 32;
+  using SM = MergeSmem<NT, IPT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  __shared__ IT s_bs[NT];
+  __shared__ int s_len[NT], s_pex[NT];
+  __shared__ double s_av[NT];
+  __shared__ int s_w[NW + 1];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    // 1. expand (lines 3-6 of Algorithm 1) into buffer 0; run starts of the nonempty b_j*
+    int u = 0, nr = 0;
+    for (int64_t e0 = a0; e0 < a1; e0 += NT) {
+      const int64_t e = e0 + tid;
+      int len = 0;
+      if (e < a1) {
+        const int j = __ldg(a.A.ci + e);
+        const int64_t b0 = __ldg(a.B.rp + j);
+        len = (int)(__ldg(a.B.rp + j + 1) - b0);
+        s_bs[tid] = (IT)b0;
+        s_av[tid] = __ldg(a.A.val + e);
+      }
+      int tot, rtot;
+      const int ex = esc_block_excl_scan<NT>(len, &tot, s_w);
+      const int rex = esc_block_excl_scan<NT>(len > 0 ? 1 : 0, &rtot, s_w);
+      s_len[tid] = len;
+      s_pex[tid] = u + ex;
+      if (len > 0) sm.rb[nr + rex] = (unsigned short)(u + ex);
+      __syncthreads();
+      const int na = (int)((a1 - e0) < NT ? (a1 - e0) : NT);
+      for (int t = w; t < na; t += NW) {
+        const IT bs = s_bs[t];
+        const int lt = s_len[t], pe = s_pex[t];
+        const double at = s_av[t];
+        for (int q = lane; q < lt; q += 32) {
+          sm.key[0][pe + q] = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
+          sm.val[0][pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
+        }
+      }
+      u += tot;
+      nr += rtot;
+      __syncthreads();
+    }
+    if (tid == 0) sm.rb[nr] = (unsigned short)u;
+    __syncthreads();
+    // 2. merge rounds (src buffer b, runs [rb[k], rb[k+1]), k < nr)
+    int b = 0;
+    while (nr > 1) {
+      const int nr2 = (nr + 1) >> 1;
+      int x = tid * IPT;
+      const int xe = min(x + IPT, u);
+      if (x < xe) {
+        // the pair holding x: largest k with rb[2k] <= x
+        int lo2 = 0, hi2 = nr2 - 1;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2 + 1) >> 1;
+          if (sm.rb[2 * mid] <= x) lo2 = mid;
+          else hi2 = mid - 1;
+        }
+        int k = lo2;
+        while (x < xe) {
+          const int l0 = sm.rb[2 * k];
+          const int l1 = 2 * k + 1 < nr ? sm.rb[2 * k + 1] : u;
+          const int r1 = 2 * k + 2 <= nr ? sm.rb[min(2 * k + 2, nr)] : u;
+          const int nl = l1 - l0, nrr = r1 - l1;
+          const int d = x - l0;
+          // merge path: i elements from the left run precede output d (left first on ties)
+          int ilo = d > nrr ? d - nrr : 0, ihi = d < nl ? d : nl;
+          while (ilo < ihi) {
+            const int mid = (ilo + ihi) >> 1;
+            if (sm.key[b][l0 + mid] <= sm.key[b][l1 + d - mid - 1]) ilo = mid + 1;
+            else ihi = mid;
+          }
+          int i = ilo, j = d - ilo;
+          const int xend = min(xe, r1);
+          for (; x < xend; ++x) {
+            const bool takel = i < nl && (j >= nrr || sm.key[b][l0 + i] <= sm.key[b][l1 + j]);
+            const int src = takel ? l0 + i : l1 + j;
+            sm.key[b ^ 1][x] = sm.key[b][src];
+            sm.val[b ^ 1][x] = sm.val[b][src];
+            i += takel ? 1 : 0;
+            j += takel ? 0 : 1;
+          }
+          ++k;
+        }
+      }
+      __syncthreads();
+      // new run starts: rb[k] = rb[2k]
+      unsigned short nb[(U + 2 + NT - 1) / NT];
+#pragma unroll
+      for (int q = 0; q < (U + 2 + NT - 1) / NT; ++q) {
+        const int k = tid + q * NT;
+        nb[q] = (k <= nr2 && 2 * k <= nr) ? sm.rb[min(2 * k, nr)] : 0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < (U + 2 + NT - 1) / NT; ++q) {
+        const int k = tid + q * NT;
+        if (k < nr2) sm.rb[k] = nb[q];
+      }
+      if (tid == 0) sm.rb[nr2] = (unsigned short)u;
+      nr = nr2;
+      b ^= 1;
+      __syncthreads();
+    }
+    // 3. compress: runs of equal columns summed left to right (lines 9, 11), written in order
+    const unsigned* key = sm.key[b];
+    const double* val = sm.val[b];
+    int heads = 0;
+    for (int i = 0; i < IPT; ++i) {
+      const int p = tid * IPT + i;
+      heads += (p < u && (p == 0 || key[p - 1] != key[p])) ? 1 : 0;
+    }
+    int nnz;
+    int pos = esc_block_excl_scan<NT>(heads, &nnz, s_w);
+    const int64_t o = __ldg(a.out_off + row);
+    for (int i = 0; i < IPT; ++i) {
+      const int p = tid * IPT + i;
+      if (p < u && (p == 0 || key[p - 1] != key[p])) {
+        double acc = val[p];
+        for (int x = p + 1; x < u && key[x] == key[p]; ++x) acc = __dadd_rn(acc, val[x]);
+        sm.key[b ^ 1][pos] = key[p];
+        sm.val[b ^ 1][pos] = acc;
+        ++pos;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < nnz; i += NT) {
+      a.out_col[o + i] = (int)sm.key[b ^ 1][i] + lo;
+      a.out_val[o + i] = sm.val[b ^ 1][i];
+    }
+    if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncthreads();
+  }
+}
+
+template <int NT, int IPT, typename IT>
+cudaError_t launch_merge_k(const Stage3Args& a, cudaStream_t s) {
+  const size_t bytes = sizeof(MergeSmem<NT, IPT>);
+  auto kern = k_esc_merge<NT, IPT, IT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = int64_t(num_sms()) * per_sm;
+  if (grid > a.count) grid = a.count;
+  kern<<<(unsigned)grid, NT, bytes, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int NT, int IPT>
 cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
   return i32 ? launch_esc_k<NT, IPT, MODE_FILL, int>(a, s) : launch_esc_k<NT, IPT, MODE_FILL, int64_t>(a, s);
 }
 
+// Merge kernels use an odd number of items per thread: each thread reads and writes its own
+// consecutive positions, so an odd stride keeps the 32 lanes on 32 different banks.
+template <int NT, int IPT>
+cudaError_t launch_merge_t(const Stage3Args& a, cudaStream_t s) {
+  const bool i32 = a.b_nnz < (int64_t(1) << 31);
+  return i32 ? launch_merge_k<NT, IPT, int>(a, s) : launch_merge_k<NT, IPT, int64_t>(a, s);
+}
+
 }  // namespace
 
-// Rows of the warp classes (u <= 0.8·S) sorted in one CTA of S items.
+// Rows of the warp classes (u <= 0.8·S) sorted in one CTA of at least S items by the run
+// merge (measured faster than the radix sort at these sizes; slower at 4096+, c3a / c5).
 cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   switch (S) {
-    case 64: return launch_esc_t<32, 2>(a, s);
-    case 128: return launch_esc_t<32, 4>(a, s);
-    case 256: return launch_esc_t<64, 4>(a, s);
-    case 512: return launch_esc_t<64, 8>(a, s);
-    case 1024: return launch_esc_t<128, 8>(a, s);
-    case 2048: return launch_esc_t<256, 8>(a, s);
+    case 64: return launch_merge_t<32, 3>(a, s);
+    case 128: return launch_merge_t<32, 5>(a, s);
+    case 256: return launch_merge_t<64, 5>(a, s);
+    case 512: return launch_merge_t<64, 9>(a, s);
+    case 1024: return launch_merge_t<128, 9>(a, s);
+    case 2048: return launch_merge_t<256, 9>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }
