@@ -124,15 +124,25 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
       }
     }
   }
-  if (__any_sync(0xffffffffu, wmax > 0)) {
+  // window maxima of the bw rows: one global atomic per block (the same two addresses for
+  // every block: per-row or per-warp atomics serialise at L2)
+  {
+    __shared__ unsigned long long s_wv[2];
+    if (threadIdx.x == 0) s_wv[0] = s_wv[1] = 0ull;
+    __syncthreads();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       wmax = max(wmax, (int64_t)__shfl_xor_sync(0xffffffffu, wmax, o));
       vmax = max(vmax, (int64_t)__shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumWmax), (unsigned long long)wmax);
-      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), (unsigned long long)vmax);
+    if ((threadIdx.x & 31) == 0 && wmax > 0) {
+      atomicMax(&s_wv[0], (unsigned long long)wmax);
+      atomicMax(&s_wv[1], (unsigned long long)vmax);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_wv[0] > 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumWmax), s_wv[0]);
+      atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), s_wv[1]);
     }
   }
   // block reductions
@@ -172,20 +182,28 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
                                               int64_t* __restrict__ blk_cap, int64_t* __restrict__ blk_usum,
                                               int64_t* __restrict__ blk_umax, int64_t* __restrict__ summary) {
   __shared__ int s_hist[NUM_TIERS];
+  __shared__ unsigned long long s_vmax;
   if (threadIdx.x < NUM_TIERS) s_hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_vmax = 0ull;
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * NT * RPT;
+  int64_t vmax = 0;
   for (int r = 0; r < RPT; ++r) {
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     if (i < m) {
       const int t = classify_exact(U[i], nnz_row[i], (int)tier[i], tp);
       tier[i] = (uint8_t)t;
       atomicAdd(&s_hist[t], 1);
-      if (t == T_BW)
-        atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), (unsigned long long)nnz_row[i]);
+      if (t == T_BW) vmax = nnz_row[i] > vmax ? nnz_row[i] : vmax;
     }
   }
+  // max nnz(c_i*) of the bw rows: one global atomic per block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vmax = max(vmax, (int64_t)__shfl_xor_sync(0xffffffffu, vmax, o));
+  if ((threadIdx.x & 31) == 0 && vmax > 0) atomicMax(&s_vmax, (unsigned long long)vmax);
   __syncthreads();
+  if (threadIdx.x == 0 && s_vmax > 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(summary + kSumVmax), s_vmax);
   if (threadIdx.x == 0) {
     blk_cap[blockIdx.x] = 0;
     blk_usum[blockIdx.x] = 0;
