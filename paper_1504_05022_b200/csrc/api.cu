@@ -614,18 +614,19 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->launches_sym += 3;
   if (precise && h->nlong > 0) h->launches_sym += 4;
   cudaEventRecord(h->ev[3], h->stream);
-  CK(h, cudaMemcpyAsync(h->pinned, h->c_rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-  s = sync(h);
-  if (s != SPGEMM_SUCCESS) return s;
-  h->nnz_c = h->pinned[0];
-  tr("long rows + scan + nnz D2H");
   if (precise) {
-    // numeric classes from the exact row lengths (tables sized by nnz(c_i*), not the bound)
+    // numeric classes from the exact row lengths (tables sized by nnz(c_i*), not the bound);
+    // launched before reading nnz(C) so one synchronisation returns both
     CK(h, launch_rebin(m, h->n, h->nnz_row, tp, ws, h->stream));
     h->launches_sym += 3;
     CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
-    s = sync(h);
-    if (s != SPGEMM_SUCCESS) return s;
+  }
+  CK(h, cudaMemcpyAsync(h->pinned + kSumLen, h->c_rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  s = sync(h);
+  if (s != SPGEMM_SUCCESS) return s;
+  h->nnz_c = h->pinned[kSumLen];
+  tr("long rows + scan + re-binning + nnz D2H");
+  if (precise) {
     for (int t = 0; t < NUM_TIERS; ++t) {
       h->tier_count[t] = h->pinned[kSumCount + t];
       h->tier_off[t] = h->pinned[kSumOff + t];
@@ -635,7 +636,6 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->long_first = h->tier_off[T_LONG];
     h->bw_vmax = h->pinned[kSumVmax];  // exact: max nnz(c_i*) over the window rows
     h->bw_bmax = h->pinned[kSumBmax];
-    tr("re-binning");
   }
   h->sym_ok = true;
   *c_nnz = h->nnz_c;
