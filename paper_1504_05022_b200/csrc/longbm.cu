@@ -262,9 +262,9 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBmNT, sm);
   if (per_sm < 1) per_sm = 1;
-  // fill: one CTA per SM keeps the rows being accumulated (fp64 atomics into C) plus B
-  // resident in L2; more concurrent rows thrash it (measured: 100 GB of DRAM traffic on c3b)
-  if (fill) per_sm = 1;
+  // fill: at most two CTAs per SM keep the rows being accumulated (fp64 atomics into C) plus
+  // B resident in L2; more concurrent rows thrash it (c3b: 1 CTA 88 ms, 2 CTAs 76, 3 CTAs 81)
+  if (fill && per_sm > 2) per_sm = 2;
   int64_t grid = int64_t(sm_count()) * per_sm;
   if (grid > a.count) grid = a.count;
   kern<<<(unsigned)grid, kBmNT, sm, s>>>(a);
