@@ -115,6 +115,9 @@ __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_cl
   if (sym_class == T_BW) return T_BW;  // window and bound unchanged: nnz <= min(u, W) <= kBwMaxV
   // warp classes: the numeric pass sorts the row's u <= 0.8·S products in one CTA (ESC)
   if (p.force_tier < 0 && sym_class >= T_W64 && sym_class <= T_W2048) return sym_class;
+  // long rows stay on the bitmap path (ranks, no sort): c3b rows with u > 8192 but
+  // nnz <= 8192 took 248 ps/product in the CTA hash vs 28 in the bitmap fill
+  if (p.force_tier < 0 && sym_class == T_LONG) return T_LONG;
   const bool has_struct = sym_class >= T_W64 && sym_class <= T_W2048;
   if (p.force_tier >= 0 && u >= 2 && tier_exact_ok(p.force_tier, u, nnz) &&
       (has_struct || p.force_tier < T_W64 || p.force_tier > T_W2048) &&
