@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
   __shared__ unsigned s_max[NW];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
-  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * rper; r < rend; ++r) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
@@ -243,7 +245,9 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
   __shared__ int s_w[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
-  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * rper; r < rend; ++r) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);

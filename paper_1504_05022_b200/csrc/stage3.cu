@@ -46,8 +46,11 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
   constexpr int GPW = 32 / G;
   const bool fill = a.mode == MODE_FILL;
 
-  for (int64_t wt = int64_t(blockIdx.x) * WPB + warp; wt * GPW < a.count;
-       wt += int64_t(gridDim.x) * WPB) {
+  // each CTA takes a contiguous range of tiles (neighbouring rows share b_j*: L1 reuse)
+  const int64_t ntiles = (a.count + GPW - 1) / GPW;
+  const int64_t tper = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t tend = min(int64_t(blockIdx.x) * tper + tper, ntiles);
+  for (int64_t wt = int64_t(blockIdx.x) * tper + warp; wt < tend; wt += WPB) {
     const int64_t gi = wt * GPW + lane / G;
     const bool has = gi < a.count;
     const int row = has ? __ldg(a.perm + a.first + gi) : 0;
@@ -209,7 +212,9 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool fill = a.mode == MODE_FILL;
 
-  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * rper; r < rend; ++r) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     // column window [lo, hi] of the row: first/last column of each b_j*

@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(NW * 32) k_wrow(Stage3Args a) {
   int* list = s_list[LIST ? w : 0];
   double* vals = s_vals[FILL ? w : 0];
 
-  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * rper + w; r < rend; r += NW) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int4* k4 = reinterpret_cast<int4*>(keys);
@@ -316,7 +318,9 @@ __global__ void __launch_bounds__(NW * 32) k_wdense(Stage3Args a) {
   int2* tab = s_tab[w];
   double* vals = s_vals[w];
 
-  for (int64_t r = int64_t(blockIdx.x) * NW + w; r < a.count; r += int64_t(gridDim.x) * NW) {
+  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * rper + w; r < rend; r += NW) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t o = __ldg(a.out_off + row);
     const int nnz = (int)(__ldg(a.out_off + row + 1) - o);
@@ -478,7 +482,11 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   int bmax = 0;  // STRUCT: most nonzero 1024-column blocks in one row (sizes DENSE's slots)
 
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;
-  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < count; r += int64_t(gridDim.x) * nw) {
+  // each CTA takes a contiguous range of the class's rows (ascending row ids): neighbouring
+  // rows share b_j*, so the CTA's warps reuse them from L1
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t rend = min(int64_t(blockIdx.x) * per + per, count);
+  for (int64_t r = int64_t(blockIdx.x) * per + w; r < rend; r += nw) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
@@ -684,7 +692,9 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
   const unsigned lt = lanemask_lt_();
   int bmax = 0;
 
-  for (int64_t r = int64_t(blockIdx.x) * nw + w; r < a.count; r += int64_t(gridDim.x) * nw) {
+  const int64_t per = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA (L1 reuse)
+  const int64_t rend = min(int64_t(blockIdx.x) * per + per, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * per + w; r < rend; r += nw) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
