@@ -125,6 +125,7 @@ struct spgemm_handle_s {
   int64_t tier_off[NUM_TIERS + 1] = {};
   int64_t sum_u = 0, max_u = 0, sum_cap = 0;
   int64_t bw_wmax = 0, bw_vmax = 0, bw_bmax = 0;  // T_BW class: largest window, row length, blocks
+  int* work_ctr = nullptr;  // long-row dynamic scheduling counter (symbolic workspace)
   bool sym_ok = false;
   int64_t nnz_c = 0;
   std::string err;
@@ -190,6 +191,7 @@ void free_symbolic(spgemm_handle_t h) {
   h->nnz_row = h->c_rp = h->scan_tmp = nullptr;
   h->ctil_col = nullptr;
   h->ctil_val = nullptr;
+  h->work_ctr = nullptr;
   h->lst = nullptr;
   h->lkeys = h->lold_keys = nullptr;
   h->lvals = h->lold_vals = nullptr;
@@ -601,6 +603,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.count = h->nlong;
     a.nnz_row = h->nnz_row;
     a.mode = MODE_COUNT;
+    AL(h, &h->work_ctr, 1);
+    a.work_ctr = h->work_ctr;
     CK(h, launch_long_bitmap(a, h->stream));
     h->launches_sym += 1;
   }
@@ -714,6 +718,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.out_col = c_col_idx;
         a.out_val = c_val;
         a.mode = MODE_FILL;
+        a.work_ctr = h->work_ctr;
         cudaEventRecord(h->tev[T_LONG][0], h->stream);
         CK(h, launch_long_bitmap(a, h->stream));
         cudaEventRecord(h->tev[T_LONG][1], h->stream);

@@ -180,6 +180,7 @@ struct Stage3Args {
   int32_t* bw_ovf_list;       // T_BW STRUCT: rows with more nonzero blocks than the slots
   int32_t* bw_ovf_cnt;        //   (re-run over the full-window bitmap; device counter)
   const int32_t* count_dev;   // if set, the kernel reads its row count here (rows = perm[0..))
+  int* work_ctr;              // long rows: dynamic row counter (zeroed by the launcher)
 };
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------

@@ -133,6 +133,16 @@ __device__ __forceinline__ void for_each_product(const Stage3Args& a, int64_t a0
   }
 }
 
+// Long rows differ by orders of magnitude in work (c3b: 8 Ki to 2.5 Mi products): CTAs take
+// their next row from a global counter instead of a fixed stride.
+__device__ __forceinline__ int64_t next_row(const Stage3Args& a, int64_t r, int64_t* s_next) {
+  if (!a.work_ctr) return r + gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) *s_next = int64_t(gridDim.x) + atomicAdd(a.work_ctr, 1);
+  __syncthreads();
+  return *s_next;
+}
+
 __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
@@ -140,7 +150,8 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
   __shared__ int s_w[kBmNT / 32 + 1];
   __shared__ BmBatch sb;
   __shared__ unsigned long long s_cnt;
-  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+  __shared__ int64_t s_next;
+  for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int lo, hi;
@@ -180,7 +191,8 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
   __shared__ int s_red[2 * (kBmNT / 32)];
   __shared__ int s_w[kBmNT / 32 + 1];
   __shared__ BmBatch sb;
-  for (int64_t r = blockIdx.x; r < a.count; r += gridDim.x) {
+  __shared__ int64_t s_next;
+  for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     const int64_t o = __ldg(a.out_off + row);
@@ -252,6 +264,10 @@ int sm_count() {
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const bool fill = a.mode == MODE_FILL;
+  if (a.work_ctr) {
+    cudaError_t e0 = cudaMemsetAsync(a.work_ctr, 0, sizeof(int), s);
+    if (e0 != cudaSuccess) return e0;
+  }
   // tiles never exceed the column range [0, n): size shared memory by it (c3b: 8 Ki words)
   const int64_t nwords = ((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT;
   const int64_t tw = nwords < kTileWords ? nwords : kTileWords;
