@@ -330,3 +330,63 @@ def test_numeric_before_symbolic():
     with pytest.raises(sg.SpgemmError):
         op.numeric()
     op.destroy()
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+def test_bw_block_directory_overflow(flags_name):
+    """Window-bitmap rows whose products touch more 1024-column blocks than the precise
+    symbolic pass has directory slots (16) are redone over the full window: a wide window
+    (n = 100 000 < 2^17) and rows of 60-200 uniform columns (≈ 50-100 nonzero blocks), mixed
+    with narrow rows that fit the directory.  Exact in int mode against the oracle."""
+    import paper_1504_05022_b200 as sg
+    n = 100_000
+    lengths = np.array([3 + (i * 7) % 5 for i in range(300)])
+    A = gen.random_rows(300, 3000, lengths, seed=11, mode="int")
+    wide = gen.random_rows(1500, n, np.array([60 + (j * 13) % 140 for j in range(1500)]), seed=12, mode="int")
+    # narrow B rows: columns inside one 1024-column block
+    narrow = gen.random_rows(1500, 1000, np.array([5 + j % 20 for j in range(1500)]), seed=13, mode="int")
+    rp = np.concatenate([wide.rp, wide.rp[-1] + narrow.rp[1:]])
+    B = gen.Csr((3000, n), rp, np.concatenate([wide.ci, narrow.ci]), np.concatenate([wide.val, narrow.val]))
+    flags = getattr(sg, flags_name) if flags_name else 0
+    g = run_gpu(A, B, flags=flags, stats=True)
+    R = oracle.spgemm(A, B)
+    compare(g, R, exact=True, what="bw overflow")
+    assert "bw" in g["stats"]["tier_rows"]
+
+
+def _wide_pair(seed, a_lens, n=400_000, k=2000, blen=64):
+    """Row i of A picks a_lens[i] rows of B, each with blen uniform columns over n > 2^17
+    (no window-bitmap rows): u_i = 64·a_lens[i] spans the w, e and long classes, with
+    about u²/2n repeated columns per row."""
+    B = gen.random_rows(k, n, np.full(k, blen), seed=seed, mode="real")
+    A = gen.random_rows(len(a_lens), k, np.array(a_lens), seed=seed + 1, mode="real")
+    return A, B
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+def test_determinism_real_all_classes(flags_name):
+    """Run-to-run bit-identical values in real mode through the w (ESC merge) and e (ESC
+    radix) classes (R1: every class but the atomic ones — CTA hash, long rows — is
+    order-fixed)."""
+    import paper_1504_05022_b200 as sg
+    flags = getattr(sg, flags_name) if flags_name else 0
+    A, B = _wide_pair(5, [1, 3, 10, 20, 40, 100] * 6)
+    g1 = run_gpu(A, B, flags=flags, stats=True)
+    g2 = run_gpu(A, B, flags=flags)
+    R = oracle.spgemm(A, B)
+    compare(g1, R, exact=False, what="real classes")
+    np.testing.assert_array_equal(g1["ci"], g2["ci"])
+    np.testing.assert_array_equal(g1["val"].view(np.int64), g2["val"].view(np.int64))
+    classes = set(g1["stats"]["tier_rows"])
+    assert any(c.startswith("w") for c in classes) and any(c.startswith("e") for c in classes), classes
+
+
+def test_esc_bitexact_vs_oracle_real():
+    """The ESC sorts (run merge for the warp classes' values, radix for e-classes) are stable
+    and sum each column left to right: values bit-identical to the oracle in real mode."""
+    import paper_1504_05022_b200 as sg
+    A, B = _wide_pair(8, [2, 10, 20, 40, 100] * 8)
+    g = run_gpu(A, B, flags=sg.FLAG_PRECISE, stats=True)
+    R = oracle.spgemm(A, B)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
