@@ -464,11 +464,13 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_BW:
       return launch_bw_tier(a, s);
     // ESC (sorted) for values; counting only needs distinct keys: the CTA hash of the same size
+    // (e4096: twice the size, load <= 1/4 — c5 count 33 -> 23 ms at 2^20; larger tables for
+    // e2048 / e8192 measured slower on c3a / c3b: clearing and occupancy)
     case T_E2048:
       if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * 4, a.count, 1, a, s);
       return launch_esc(tier, a, s);
     case T_E4096:
-      if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * 4, a.count, 1, a, s);
+      if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * 4, a.count, 1, a, s);
       return launch_esc(tier, a, s);
     case T_E8192:
       if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * 4, a.count, 1, a, s);
