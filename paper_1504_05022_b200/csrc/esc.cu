@@ -235,7 +235,8 @@ template <int NT, int IPT>
 struct MergeSmem {
   static constexpr int U = NT * IPT;
   unsigned key[2][U];
-  double val[2][U];
+  unsigned short idx[2][U];  // product position p: values stay in pval until the compression
+  double pval[U];
   unsigned short rb[U + 2];  // run boundaries (nonempty runs)
 };
 
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
         const double at = s_av[t];
         for (int q = lane; q < lt; q += 32) {
           sm.key[0][pe + q] = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
-          sm.val[0][pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
+          sm.idx[0][pe + q] = (unsigned short)(pe + q);
+          sm.pval[pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
         }
       }
       u += tot;
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
             const bool takel = i < nl && (j >= nrr || sm.key[b][l0 + i] <= sm.key[b][l1 + j]);
             const int src = takel ? l0 + i : l1 + j;
             sm.key[b ^ 1][x] = sm.key[b][src];
-            sm.val[b ^ 1][x] = sm.val[b][src];
+            sm.idx[b ^ 1][x] = sm.idx[b][src];
             i += takel ? 1 : 0;
             j += takel ? 0 : 1;
           }
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
     }
     // 3. compress: runs of equal columns summed left to right (lines 9, 11), written in order
     const unsigned* key = sm.key[b];
-    const double* val = sm.val[b];
+    const unsigned short* idx = sm.idx[b];
     int heads = 0;
     for (int i = 0; i < IPT; ++i) {
       const int p = tid * IPT + i;
@@ -364,20 +366,28 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
     int nnz;
     int pos = esc_block_excl_scan<NT>(heads, &nnz, s_w);
     const int64_t o = __ldg(a.out_off + row);
+    double vh[IPT];
     for (int i = 0; i < IPT; ++i) {
       const int p = tid * IPT + i;
       if (p < u && (p == 0 || key[p - 1] != key[p])) {
-        double acc = val[p];
-        for (int x = p + 1; x < u && key[x] == key[p]; ++x) acc = __dadd_rn(acc, val[x]);
+        double acc = sm.pval[idx[p]];
+        for (int x = p + 1; x < u && key[x] == key[p]; ++x) acc = __dadd_rn(acc, sm.pval[idx[x]]);
+        vh[i] = acc;
+      }
+    }
+    __syncthreads();  // all reads of the sorted buffer done: compact in place of the other one
+    for (int i = 0; i < IPT; ++i) {
+      const int p = tid * IPT + i;
+      if (p < u && (p == 0 || key[p - 1] != key[p])) {
         sm.key[b ^ 1][pos] = key[p];
-        sm.val[b ^ 1][pos] = acc;
+        sm.pval[pos] = vh[i];
         ++pos;
       }
     }
     __syncthreads();
     for (int i = tid; i < nnz; i += NT) {
       a.out_col[o + i] = (int)sm.key[b ^ 1][i] + lo;
-      a.out_val[o + i] = sm.val[b ^ 1][i];
+      a.out_val[o + i] = sm.pval[i];
     }
     if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncthreads();
