@@ -347,7 +347,7 @@ def run_gpu(args):
             dense = (not hybrid) and cls_name == "bw"
             alg = (36 if dense else 28) * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + \
                 12 * c["c_entries"] + (4 * c["c_entries"] if dense else 0)
-            kname = "k_bwrow" if cls_name == "bw" else \
+            kname = "k_bwrow / k_bw_struct2" if cls_name == "bw" else \
                 "k_esc_sort" if cls_name.startswith("w") else \
                 "k_group" if cls_name.startswith("g") else "k_esc_sort" if cls_name.startswith("e") else \
                 "k_cta_hash" if cls_name.startswith("c") else ("k_long" if hybrid else "k_long_bm_fill")

@@ -572,7 +572,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.bw_wmax = h->bw_wmax;
     a.bw_vmax = h->bw_vmax;
     a.bw_bmax_out = ws.summary + kSumBmax;
-    if (t == T_BW && !hybrid) {
+    if (t == T_BW) {
       AL(h, &a.bw_ovf_list, h->tier_count[T_BW]);
       AL(h, &a.bw_ovf_cnt, 1);
     }

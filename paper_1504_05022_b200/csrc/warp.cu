@@ -665,32 +665,37 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
 // bitmap slot (allocated on first touch, warp-synchronously: the lanes of one b_j* hold
 // ascending columns, so each newly touched block is claimed by the first lane of its run).
 // Per warp: dir uint16[nsw] (block -> slot + 1) | bits uint32[ns·32].  ~2.3 KB per warp
-// instead of W/8: 2x the resident warps on c2.  Inserting is a fire-and-forget shared OR.  A row touching more than ns blocks is appended to an overflow list and redone by the
-// full-window kernel.
+// instead of W/8: 2x the resident warps on c2.  Inserting is a fire-and-forget shared OR.
+// A row touching more than ns blocks is appended to an overflow list and redone by the
+// full-window kernel.  FILL (hybrid) continues like the DENSE numeric kernel: ranks per word
+// from the emission, a second walk adds each product at its rank (c2 hybrid 20.3 -> 15.0 ms).
+// FILL (hybrid) adds pre uint16[ns·32] (rank of each word's first bit) and vals double[nv+1].
 struct Bs2Layout {
-  int nsw, ns;
-  unsigned o_bits, o_wmask, bytes;
+  int nsw, ns, nv;
+  unsigned o_bits, o_pre, o_vals, bytes;
 };
 
-__host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns) {
+__host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns, bool fill, int64_t vmax) {
   Bs2Layout L;
   const int nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
   L.nsw = (nwd / 32 + 31) / 32 * 32;
   L.ns = ns;
+  L.nv = (int)(vmax > 0 ? vmax : 1);
   L.o_bits = (2u * L.nsw + 15u) & ~15u;
-  L.o_wmask = L.o_bits + 128u * ns;
-  L.bytes = L.o_wmask;
+  L.o_pre = L.o_bits + 128u * ns;
+  L.o_vals = L.o_pre + (fill ? 64u * ns : 0u);
+  L.bytes = fill ? ((L.o_vals + 8u * (L.nv + 1) + 15u) & ~15u) : L.o_pre;
   return L;
 }
 
-template <typename IT>
+template <typename IT, bool FILL>
 __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
-  const unsigned bits = dir + L.o_bits;
+  const unsigned bits = dir + L.o_bits, pre = dir + L.o_pre, vals = dir + L.o_vals;
   const int ns = L.ns, nsw = L.nsw;
-  for (unsigned i = lane; i < L.bytes / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
+  for (unsigned i = lane; i < L.o_pre / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
   __syncwarp();
   const unsigned lt = lanemask_lt_();
   int bmax = 0;
@@ -736,17 +741,18 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     for (int s0 = 0; s0 < nsw; s0 += 32) {
       const unsigned dl = sh_ld_u16(dir + 2u * (s0 + lane));
       unsigned nzb = __ballot_sync(kFull, dl != 0u);
-      if (dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
+      if (!FILL && dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
       while (nzb) {
         const int b = __ffs(nzb) - 1;
         nzb &= nzb - 1;
         const unsigned slot = __shfl_sync(kFull, dl, b) - 1u;
         const unsigned wa = bits + 4u * (slot * 32u + lane);
         unsigned word = sh_ld(wa);
-        if (word) sh_st(wa, 0u);
+        if (!FILL && word) sh_st(wa, 0u);
         const int pc = __popc(word);
         const int inc = warp_incl_scan(pc, lane);
         int p = nnz + inc - pc;
+        if (FILL) sh_st_u16(pre + 2u * (slot * 32u + lane), (unsigned)p);
         const int cb = lo + ((s0 + b) * 32 + lane) * 32;
         while (word) {
           oc[p++] = cb + __ffs(word) - 1;
@@ -754,6 +760,25 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
         }
         nnz += __shfl_sync(kFull, inc, 31);
       }
+    }
+    if (FILL) {
+      // lines 6, 9, 11: values at the columns' ranks (as the DENSE numeric kernel), then clear
+      for (int p = lane; p < nnz; p += 32) sh_st_f64(vals + 8u * p, -0.0);
+      __syncwarp();
+      const unsigned scratch = vals + 8u * unsigned(L.nv);
+      walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
+        const unsigned d = act ? (unsigned)(c - lo) : 0u;
+        const unsigned wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
+        const unsigned word = sh_ld(bits + 4u * wi);
+        const unsigned rank = sh_ld_u16(pre + 2u * wi) + __popc(word & ((1u << (d & 31)) - 1u));
+        const unsigned va = act ? vals + 8u * rank : scratch;
+        sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
+      });
+      __syncwarp();
+      double* ov = a.out_val + o;
+      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
+      for (int sl = 0; sl < nslot; ++sl) sh_st(bits + 4u * (unsigned(sl) * 32u + lane), 0u);
+      for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
     bmax = max(bmax, nslot);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
@@ -851,10 +876,10 @@ static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
 
 constexpr int kBs2Slots = 16;
 
-template <typename IT>
+template <typename IT, bool FILL>
 static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
-  const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots);
-  auto kern = k_bw_struct2<IT>;
+  const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots, FILL, a.bw_vmax);
+  auto kern = k_bw_struct2<IT, FILL>;
   constexpr int nw = 8;
   const size_t bytes = size_t(nw) * L.bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -873,19 +898,22 @@ cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const int64_t blocks = (a.bw_wmax + 1023) / 1024;
   static const bool no_bs2 = getenv("SPGEMM_NO_BS2") != nullptr;  // A/B switch (development)
-  if (a.mode == MODE_STRUCT && blocks > kBs2Slots && a.bw_ovf_list && a.bw_ovf_cnt && !no_bs2) {
+  const bool dir_mode = a.mode == MODE_STRUCT || a.mode == MODE_FILL;
+  if (dir_mode && blocks > kBs2Slots && a.bw_ovf_list && a.bw_ovf_cnt && !no_bs2) {
     // block-directory pass, then the full-window pass over the rows that overflowed it
     cudaError_t e = cudaMemsetAsync(a.bw_ovf_cnt, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     const bool i32 = a.b_nnz < (int64_t(1) << 31);
-    e = i32 ? launch_bs2<int>(a, s) : launch_bs2<int64_t>(a, s);
+    const bool fill = a.mode == MODE_FILL;
+    e = fill ? (i32 ? launch_bs2<int, true>(a, s) : launch_bs2<int64_t, true>(a, s))
+             : (i32 ? launch_bs2<int, false>(a, s) : launch_bs2<int64_t, false>(a, s));
     if (e != cudaSuccess) return e;
     Stage3Args b = a;
     b.perm = a.bw_ovf_list;
     b.first = 0;
     b.count = a.count;  // grid bound; the kernel reads the real count from count_dev
     b.count_dev = a.bw_ovf_cnt;
-    return launch_bw_mode<MODE_STRUCT>(b, s);
+    return fill ? launch_bw_mode<MODE_FILL>(b, s) : launch_bw_mode<MODE_STRUCT>(b, s);
   }
   switch (a.mode) {
     case MODE_FILL: return launch_bw_mode<MODE_FILL>(a, s);
