@@ -804,7 +804,9 @@ static cudaError_t launch_warp_kernel(K kernel, int nw, int64_t rows, const Stag
   return cudaGetLastError();
 }
 
-// Warp classes T_W64..T_W2048: S = 64 << (tier - T_W64) slots.  Warps per block: as many as
+// Warp classes T_W64..T_W2048: S = 64 << (tier - T_W64) slots; COUNT uses 2S for S <= 512
+// (load <= 0.4 instead of 0.8: c3a w64..w512 counts 1.6x faster; at 1024/2048 the halved
+// occupancy cancels the shorter probes).  Warps per block: as many as
 // the 48 KB static shared-memory limit allows (per warp: COUNT 4S, STRUCT 8S, FILL 16S,
 // DENSE 12S bytes), at most 8.
 cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s) {
@@ -813,20 +815,21 @@ cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s) {
 #define SG_W(LOG2S)                                                                           \
   {                                                                                           \
     constexpr int S_ = 1 << LOG2S;                                                            \
-    constexpr int NC = SG_NW(4 * S_), NS = SG_NW(8 * S_), NF = SG_NW(16 * S_), ND = SG_NW(12 * S_); \
+    constexpr int LC = LOG2S <= 9 ? LOG2S + 1 : LOG2S;                                              \
+    constexpr int NC = SG_NW(4 << LC), NS = SG_NW(8 * S_), NF = SG_NW(16 * S_), ND = SG_NW(12 * S_); \
     if (i32) {                                                                                \
       switch (a.mode) {                                                                       \
         case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int>, ND, a.count, a, s); \
         case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int>, NF, a.count, a, s); \
         case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int>, NS, a.count, a, s); \
-        default: return launch_warp_kernel(k_wrow<LOG2S, NC, MODE_COUNT, int>, NC, a.count, a, s); \
+        default: return launch_warp_kernel(k_wrow<LC, NC, MODE_COUNT, int>, NC, a.count, a, s); \
       }                                                                                       \
     }                                                                                         \
     switch (a.mode) {                                                                         \
       case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int64_t>, ND, a.count, a, s); \
       case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int64_t>, NF, a.count, a, s); \
       case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int64_t>, NS, a.count, a, s); \
-      default: return launch_warp_kernel(k_wrow<LOG2S, NC, MODE_COUNT, int64_t>, NC, a.count, a, s); \
+      default: return launch_warp_kernel(k_wrow<LC, NC, MODE_COUNT, int64_t>, NC, a.count, a, s); \
     }                                                                                         \
   }
   switch (tier) {
