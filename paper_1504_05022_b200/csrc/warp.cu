@@ -482,10 +482,12 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   int bmax = 0;  // STRUCT: most nonzero 1024-column blocks in one row (sizes DENSE's slots)
 
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;
-  // each CTA takes a contiguous range of the class's rows (ascending row ids): neighbouring
-  // rows share b_j*, so the CTA's warps reuse them from L1.  FILL (hybrid) keeps the strided
-  // order (measured: its large per-warp buffers leave little L1; contiguous was 30 % slower).
-  const bool contig = MODE != MODE_FILL;
+  // STRUCT / COUNT: each CTA takes a contiguous range of the class's rows (ascending row
+  // ids): neighbouring rows share b_j*, reused from L1.  FILL (hybrid) and DENSE keep the
+  // strided order: FILL's large per-warp buffers leave little L1 (contiguous was 30 % slower);
+  // DENSE runs in the same time either way, but strided rows keep a 3D stencil's z-neighbours
+  // in L2 (c2 DRAM reads 2.7 GB instead of 7.5 GB, ≈ the algorithmic bytes).
+  const bool contig = MODE != MODE_FILL && MODE != MODE_DENSE;
   const int64_t per = contig ? (count + gridDim.x - 1) / gridDim.x : count;
   const int64_t rend = contig ? min(int64_t(blockIdx.x) * per + per, count) : count;
   const int64_t rstep = contig ? nw : int64_t(gridDim.x) * nw;
