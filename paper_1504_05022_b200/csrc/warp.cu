@@ -413,6 +413,11 @@ __device__ __forceinline__ int4 sh_ld_v4(unsigned addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
   return r;
 }
+__device__ __forceinline__ uint2 sh_ld_v2(unsigned addr) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr) : "memory");
+  return r;
+}
 __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
 }
@@ -444,11 +449,10 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
   unsigned off;
   if (mode == MODE_DENSE) {
     L.o_sm = 0;                                  // dir
-    off = (2u * L.nsw + 15u) & ~15u;             // bits
+    off = (2u * L.nsw + 15u) & ~15u;             // records {bits, rank} per slot word (8 B)
     L.o_lst = off;
-    off += 128u * L.ns;
-    L.o_pre = off;
-    off += 64u * L.ns;
+    off += 256u * L.ns;
+    L.o_pre = off;                               // (end of the zeroed region)
     L.o_vals = off;
     off += 8u * (L.nv + 1);  // + scratch
   } else {
@@ -618,8 +622,8 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
           a.out_col[o + p] = c;
           if (newblk) sh_st_u16(dir + 2u * (d >> 10), (unsigned)(slot + 1));
           const unsigned wi = unsigned(slot) * 32u + ((d >> 5) & 31);
-          sh_red_or(bits + 4u * wi, 1u << (d & 31));
-          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st_u16(pre + 2u * wi, (unsigned)p);
+          sh_red_or(bits + 8u * wi, 1u << (d & 31));
+          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st(bits + 8u * wi + 4u, (unsigned)p);
         }
         nslot += __popc(nm);
         prevd = __shfl_sync(kFull, d, 31);
@@ -634,14 +638,18 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     const unsigned scratch = vals + 8u * unsigned(L.nv);
     walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
-      unsigned wi;
-      if (MODE == MODE_DENSE) {
-        wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
+      unsigned word, base;
+      if (MODE == MODE_DENSE) {  // one 8-byte record: the word's bits and its first rank
+        const unsigned wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
+        const uint2 rec = sh_ld_v2(bits + 8u * wi);
+        word = rec.x;
+        base = rec.y;
       } else {
-        wi = d >> 5;
+        const unsigned wi = d >> 5;
+        word = sh_ld(bm + 4u * wi);
+        base = sh_ld_u16(pre + 2u * wi);
       }
-      const unsigned word = sh_ld((MODE == MODE_DENSE ? bits : bm) + 4u * wi);
-      const unsigned rank = sh_ld_u16(pre + 2u * wi) + __popc(word & ((1u << (d & 31)) - 1u));
+      const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
       sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
     });
@@ -651,7 +659,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     if (MODE == MODE_FILL) {
       for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
     } else {
-      for (int s = 0; s < nslot; ++s) sh_st(bits + 4u * (unsigned(s) * 32u + lane), 0u);
+      for (int s = 0; s < nslot; ++s) sh_st(bits + 8u * (unsigned(s) * 32u + lane), 0u);
       for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
