@@ -9,7 +9,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libspgemm.so")
+# SPGEMM_LIB: an alternative in-tree build (A/B timing during development); default libspgemm.so
+LIB_PATH = os.path.join(PKG, os.environ.get("SPGEMM_LIB", "libspgemm.so"))
 NUM_TIERS = 21
 
 TIER_NAMES = ["empty", "g1", "g2", "g4", "g8", "g16", "g32", "w64", "w128", "w256", "w512", "w1024",
