@@ -173,7 +173,7 @@ struct Stage3Args {
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
   const int32_t* rlo;         // first column of each row's window (stage 1)
-  const int2* bwin;           // (first, last) column of each row of B (stage 1)
+  const int4* bwin;           // (first, last, nnz) of each row of B (stage 1)
   int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
   int64_t bw_bmax;            // T_BW numeric: most nonzero 1024-column blocks in a row
   int64_t* bw_bmax_out;       // T_BW STRUCT: device max of the above (summary entry)
@@ -194,7 +194,7 @@ struct Stage12Ws {
   int64_t* blk_usum;   // [nblk]
   int64_t* blk_umax;   // [nblk]
   int64_t* summary;    // [kSumLen] device
-  int2* bwin;          // [k] (min, max) column of each row of B; (INT_MAX, -1) if empty
+  int4* bwin;          // [k] (first column, last column, nnz, 0) of each row of B
   int32_t* rlo;        // [m] first column of each row's window
   int64_t nblk;
 };

@@ -55,19 +55,21 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* total, in
 }
 
 // ---------------------------------------------------------------------------- stage 1
-// Per row j of B: its first and last column, (INT_MAX, -1) when empty (rows are sorted, Q3).
+// Per row j of B one 16-byte record: first and last column ((INT_MAX, -1) when empty; rows
+// are sorted, Q3) and nnz(b_j*) — stage 1 then gathers one record per a_ij instead of two row
+// pointers and a window pair.
 __global__ void k_bwin(int64_t k, const int64_t* __restrict__ brp, const int32_t* __restrict__ bci,
-                       int2* __restrict__ bwin) {
+                       int4* __restrict__ bwin) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= k) return;
   const int64_t b0 = __ldg(brp + j), b1 = __ldg(brp + j + 1);
-  bwin[j] = b1 > b0 ? make_int2(__ldg(bci + b0), __ldg(bci + b1 - 1)) : make_int2(INT_MAX, -1);
+  bwin[j] = b1 > b0 ? make_int4(__ldg(bci + b0), __ldg(bci + b1 - 1), (int)(b1 - b0), 0)
+                    : make_int4(INT_MAX, -1, 0, 0);
 }
 
-__device__ __forceinline__ void acc_row(int64_t& u, int& lo, int& hi, const int64_t* brp, const int2* bwin,
-                                        int j) {
-  u += __ldg(brp + j + 1) - __ldg(brp + j);  // line 4: u_i += nnz(b_j*)
-  const int2 w = __ldg(bwin + j);
+__device__ __forceinline__ void acc_row(int64_t& u, int& lo, int& hi, const int4* bwin, int j) {
+  const int4 w = __ldg(bwin + j);
+  u += w.z;  // line 4: u_i += nnz(b_j*)
   lo = min(lo, w.x);
   hi = max(hi, w.y);
 }
@@ -77,7 +79,7 @@ __device__ __forceinline__ void acc_row(int64_t& u, int& lo, int& hi, const int6
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
                                                const int64_t* __restrict__ brp,
-                                               const int2* __restrict__ bwin, TierParams tp,
+                                               const int4* __restrict__ bwin, TierParams tp,
                                                int hybrid, int64_t* __restrict__ U,
                                                uint8_t* __restrict__ tier, int32_t* __restrict__ rlo,
                                                int32_t* __restrict__ blk_tier,
@@ -102,12 +104,12 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
       for (; p + 4 <= a1; p += 4) {                      // line 3: each a_ij in a_i*
         const int j0 = __ldg(A.ci + p), j1 = __ldg(A.ci + p + 1);
         const int j2 = __ldg(A.ci + p + 2), j3 = __ldg(A.ci + p + 3);
-        acc_row(u, lo, hi, brp, bwin, j0);
-        acc_row(u, lo, hi, brp, bwin, j1);
-        acc_row(u, lo, hi, brp, bwin, j2);
-        acc_row(u, lo, hi, brp, bwin, j3);
+        acc_row(u, lo, hi, bwin, j0);
+        acc_row(u, lo, hi, bwin, j1);
+        acc_row(u, lo, hi, bwin, j2);
+        acc_row(u, lo, hi, bwin, j3);
       }
-      for (; p < a1; ++p) acc_row(u, lo, hi, brp, bwin, __ldg(A.ci + p));
+      for (; p < a1; ++p) acc_row(u, lo, hi, bwin, __ldg(A.ci + p));
       const int64_t W = hi >= lo ? int64_t(hi) - lo + 1 : 0;
       const int t = classify(u, n, tp, W);
       U[i] = u;
