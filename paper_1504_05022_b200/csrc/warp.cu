@@ -1,22 +1,16 @@
-// warp.cu — stage 3, warp classes w64..w2048: one warp per row, an S-slot shared-memory
-// hash ("computing the resulting matrix", [P:262-284]; Algorithm 1 lines 3-11 [P:121-135]).
+// warp.cu — stage 3 warp-per-row classes ("computing the resulting matrix", [P:262-284];
+// Algorithm 1 lines 3-11 [P:121-135]).
 //
 // Lanes walk the rows b_j* of the row's a_ij in j-ascending order, one b_j* (up to 32 of its
-// entries) per instruction.  Columns inside one b_j* are distinct, so no two lanes of one
-// instruction insert or accumulate into one slot: the values of a column are added in
-// j-ascending order from the identity -0.0, i.e. the oracle's rounding (R1),
-// deterministic and without value atomics.
+// entries) per instruction (walk_row); the loads of four consecutive b_j* are issued before
+// their inserts.  Columns inside one b_j* are distinct, so no two lanes of one instruction
+// insert or accumulate into one slot: values of a column are added in j-ascending order from
+// the identity -0.0, i.e. the oracle's rounding (R1), without value atomics.
 //
-// The loads of four consecutive b_j* are issued before their inserts (memory-level
-// parallelism of 4 per warp); rows whose chunk holds a b_j* longer than 32 take a generic
-// loop with the same order.  New keys are appended to a per-warp list as they are claimed,
-// so the sorted output needs no compaction pass over the table.
-//
-//   MODE_COUNT   insert keys, count                              (precise symbolic)
-//   MODE_STRUCT  insert keys, count, emit the sorted key set     (precise symbolic)
-//   MODE_FILL    insert + accumulate, emit the sorted row         (hybrid: C~)
-//   MODE_DENSE   precise numeric: look columns up in a read-only key -> position table built
-//                from the STRUCT set; accumulate into a dense array already in column order.
+//   k_wrow          w64..w2048 counting: S-slot linear-probing hash (precise symbolic)
+//   k_bw_struct2    bw rows, block directory: STRUCT (precise symbolic) and FILL (hybrid)
+//   k_bwrow         bw rows over the full window: DENSE (precise numeric, from the STRUCT
+//                   set), and the STRUCT / FILL fallback for rows with too many blocks
 #include <climits>
 #include <cstdlib>
 
@@ -77,105 +71,6 @@ __device__ __forceinline__ unsigned winsert(int* keys, int* list, int& cnt, int 
     if (!__any_sync(kFull, pend)) break;
   }
   return h;
-}
-
-// Read-only lookup of a key that is known to be present.
-template <int LOG2S>
-__device__ __forceinline__ int2 wlookup(const int2* tab, int c, bool act) {
-  constexpr unsigned MASK = (1u << LOG2S) - 1;
-  unsigned h = whash<LOG2S>(c);
-  int2 kv = tab[h];
-  bool pend = act && kv.x != c;
-  while (__any_sync(kFull, pend)) {
-    if (pend) {
-      h = (h + 1) & MASK;
-      kv = tab[h];
-      pend = kv.x != c;
-    }
-  }
-  return kv;
-}
-
-// Register bitonic sort of N = 32·E int keys in "blocked" layout (lane l holds l·E .. l·E+E-1).
-template <int E>
-__device__ __forceinline__ void bitonic_blocked(int (&k)[E], int lane) {
-  constexpr int N = 32 * E;
-#pragma unroll
-  for (int kk = 2; kk <= N; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= E) {
-        const int lj = j / E;
-        const bool lower = (lane & lj) == 0;
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const bool asc = ((lane * E + r) & kk) == 0;
-          const int p = __shfl_xor_sync(kFull, k[r], lj);
-          k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          if (r & j) continue;
-          const bool asc = ((lane * E + r) & kk) == 0;
-          const int x = k[r], y = k[r | j];
-          k[r] = asc ? min(x, y) : max(x, y);
-          k[r | j] = asc ? max(x, y) : min(x, y);
-        }
-      }
-    }
-  }
-}
-
-// Sort list[0, cnt) ascending in place (registers for cnt <= 128, shared-memory bitonic above;
-// list must have room for the next power of two).
-__device__ __forceinline__ void warp_sort_list(int* list, int cnt, int lane) {
-  if (cnt <= 32) {
-    int k[1];
-    k[0] = lane < cnt ? list[lane] : INT_MAX;
-    bitonic_blocked<1>(k, lane);
-    __syncwarp();
-    if (lane < cnt) list[lane] = k[0];
-  } else if (cnt <= 64) {
-    int k[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) k[r] = lane * 2 + r < cnt ? list[lane * 2 + r] : INT_MAX;
-    bitonic_blocked<2>(k, lane);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-      if (lane * 2 + r < cnt) list[lane * 2 + r] = k[r];
-  } else if (cnt <= 128) {
-    int k[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) k[r] = lane * 4 + r < cnt ? list[lane * 4 + r] : INT_MAX;
-    bitonic_blocked<4>(k, lane);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-      if (lane * 4 + r < cnt) list[lane * 4 + r] = k[r];
-  } else {
-    int N = 1;
-    while (N < cnt) N <<= 1;
-    for (int s = cnt + lane; s < N; s += 32) list[s] = INT_MAX;
-    __syncwarp();
-    for (int kk = 2; kk <= N; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < (N >> 1); i += 32) {
-          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-          const int hi = lo + j;
-          const bool asc = (lo & kk) == 0;
-          const int kl = list[lo], kh = list[hi];
-          if ((kl > kh) == asc) {
-            list[lo] = kh;
-            list[hi] = kl;
-          }
-        }
-        __syncwarp();
-      }
-    }
-  }
-  __syncwarp();
 }
 
 // One a_ij chunk (up to 32 entries of row i of A): lane e holds b_j*'s start and length and a_ij.
@@ -248,19 +143,14 @@ __device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_
   }
 }
 
-// COUNT / STRUCT / FILL.  Shared memory per warp: keys[S], list[S], FILL: vals[S].
-template <int LOG2S, int NW, int MODE, typename IT>
+// Counting (precise symbolic, rows with W > 2^17): an S-slot table per warp, nnz = the
+// number of claimed slots.  Values of these rows are computed by the ESC (esc.cu).
+template <int LOG2S, int NW, typename IT>
 __global__ void __launch_bounds__(NW * 32) k_wrow(Stage3Args a) {
-  constexpr bool FILL = MODE == MODE_FILL;
-  constexpr bool LIST = MODE != MODE_COUNT;
   constexpr int S = 1 << LOG2S;
   __shared__ __align__(16) int s_keys[NW][S];
-  __shared__ __align__(16) int s_list[LIST ? NW : 1][LIST ? S : 1];
-  __shared__ __align__(16) double s_vals[FILL ? NW : 1][FILL ? S : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int* keys = s_keys[w];
-  int* list = s_list[LIST ? w : 0];
-  double* vals = s_vals[FILL ? w : 0];
 
   const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
   const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
@@ -270,86 +160,16 @@ __global__ void __launch_bounds__(NW * 32) k_wrow(Stage3Args a) {
     int4* k4 = reinterpret_cast<int4*>(keys);
 #pragma unroll
     for (int s = lane; s < S / 4; s += 32) k4[s] = make_int4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
-    if (FILL) {
-      double2* v2 = reinterpret_cast<double2*>(vals);
-#pragma unroll
-      for (int s = lane; s < S / 2; s += 32) v2[s] = make_double2(-0.0, -0.0);  // -0.0 + x == x
-    }
     __syncwarp();
     int cnt = 0;
-    walk_row<FILL, IT>(a, a0, a1, lane, [=, &cnt](int c, double v, double at, bool act) {
-      const unsigned h = winsert<LOG2S, LIST>(keys, list, cnt, c, act);  // lines 7-8 / 10
-      if (FILL) {
-        if (act) vals[h] = __dadd_rn(vals[h], __dmul_rn(at, v));  // lines 6, 9, 11
-        __syncwarp();
-      }
+    walk_row<false, IT>(a, a0, a1, lane, [=, &cnt](int c, double, double, bool act) {
+      winsert<LOG2S, false>(keys, nullptr, cnt, c, act);  // lines 7-8 / 10
     });
     __syncwarp();
-    if (MODE == MODE_COUNT) {
-      if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
-      __syncwarp();
-      continue;
-    }
-    warp_sort_list(list, cnt, lane);
-    const int64_t o = __ldg(a.out_off + row);
-    for (int t = lane; t < cnt; t += 32) {
-      const int c = list[t];
-      a.out_col[o + t] = c;
-      if (FILL) {
-        constexpr unsigned MASK = S - 1;
-        unsigned h = whash<LOG2S>(c);
-        while (keys[h] != c) h = (h + 1) & MASK;
-        a.out_val[o + t] = vals[h];
-      }
-    }
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
     __syncwarp();
   }
 }
-
-// PRECISE numeric: the sorted column set of row i is at struct_col + struct_off[i].
-template <int LOG2S, int NW, typename IT>
-__global__ void __launch_bounds__(NW * 32) k_wdense(Stage3Args a) {
-  constexpr int S = 1 << LOG2S;
-  constexpr unsigned MASK = S - 1;
-  __shared__ __align__(16) int2 s_tab[NW][S];
-  __shared__ __align__(16) double s_vals[NW][S / 2];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int2* tab = s_tab[w];
-  double* vals = s_vals[w];
-
-  const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
-  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
-  for (int64_t r = int64_t(blockIdx.x) * rper + w; r < rend; r += NW) {
-    const int row = __ldg(a.perm + a.first + r);
-    const int64_t o = __ldg(a.out_off + row);
-    const int nnz = (int)(__ldg(a.out_off + row + 1) - o);
-    const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
-    int4* t4 = reinterpret_cast<int4*>(tab);
-#pragma unroll
-    for (int s = lane; s < S / 2; s += 32) t4[s] = make_int4(kEmptyKey, 0, kEmptyKey, 0);
-    for (int p = lane; p < nnz; p += 32) vals[p] = -0.0;  // identity of +: first add == line 9
-    __syncwarp();
-    for (int p = lane; p < nnz; p += 32) {
-      const int c = __ldg(sc + p);
-      a.out_col[o + p] = c;  // C's columns: the sorted set itself
-      unsigned h = whash<LOG2S>(c);
-      while (atomicCAS(&tab[h].x, kEmptyKey, c) != kEmptyKey) h = (h + 1) & MASK;
-      tab[h].y = p;
-    }
-    __syncwarp();
-    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
-      const int2 kv = wlookup<LOG2S>(tab, c, act);
-      if (act) vals[kv.y] = __dadd_rn(vals[kv.y], __dmul_rn(at, v));  // line 11
-      __syncwarp();
-    });
-    __syncwarp();
-    for (int p = lane; p < nnz; p += 32) a.out_val[o + p] = vals[p];
-    __syncwarp();
-  }
-}
-
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 #pragma unroll
@@ -814,34 +634,21 @@ static cudaError_t launch_warp_kernel(K kernel, int nw, int64_t rows, const Stag
   return cudaGetLastError();
 }
 
-// Warp classes T_W64..T_W2048: S = 64 << (tier - T_W64) slots; COUNT uses 2S for S <= 512
+// Warp classes T_W64..T_W2048: S = 64 << (tier - T_W64) slots; the count uses 2S for S <= 512
 // (load <= 0.4 instead of 0.8: c3a w64..w512 counts 1.6x faster; at 1024/2048 the halved
-// occupancy cancels the shorter probes).  Warps per block: as many as
-// the 48 KB static shared-memory limit allows (per warp: COUNT 4S, STRUCT 8S, FILL 16S,
-// DENSE 12S bytes), at most 8.
+// occupancy cancels the shorter probes).  Warps per block: as many as the 48 KB static
+// shared-memory limit allows, at most 8.
 cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
 #define SG_NW(BYTES) ((49152 / (BYTES)) < 8 ? (49152 / (BYTES)) : 8)
 #define SG_W(LOG2S)                                                                           \
   {                                                                                           \
-    constexpr int S_ = 1 << LOG2S;                                                            \
-    constexpr int LC = LOG2S <= 9 ? LOG2S + 1 : LOG2S;                                              \
-    constexpr int NC = SG_NW(4 << LC), NS = SG_NW(8 * S_), NF = SG_NW(16 * S_), ND = SG_NW(12 * S_); \
-    if (i32) {                                                                                \
-      switch (a.mode) {                                                                       \
-        case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int>, ND, a.count, a, s); \
-        case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int>, NF, a.count, a, s); \
-        case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int>, NS, a.count, a, s); \
-        default: return launch_warp_kernel(k_wrow<LC, NC, MODE_COUNT, int>, NC, a.count, a, s); \
-      }                                                                                       \
-    }                                                                                         \
-    switch (a.mode) {                                                                         \
-      case MODE_DENSE: return launch_warp_kernel(k_wdense<LOG2S, ND, int64_t>, ND, a.count, a, s); \
-      case MODE_FILL: return launch_warp_kernel(k_wrow<LOG2S, NF, MODE_FILL, int64_t>, NF, a.count, a, s); \
-      case MODE_STRUCT: return launch_warp_kernel(k_wrow<LOG2S, NS, MODE_STRUCT, int64_t>, NS, a.count, a, s); \
-      default: return launch_warp_kernel(k_wrow<LC, NC, MODE_COUNT, int64_t>, NC, a.count, a, s); \
-    }                                                                                         \
+    constexpr int LC = LOG2S <= 9 ? LOG2S + 1 : LOG2S;                                        \
+    constexpr int NC = SG_NW(4 << LC);                                                        \
+    return i32 ? launch_warp_kernel(k_wrow<LC, NC, int>, NC, a.count, a, s)                  \
+               : launch_warp_kernel(k_wrow<LC, NC, int64_t>, NC, a.count, a, s);             \
   }
+  if (a.mode != MODE_COUNT) return cudaErrorInvalidValue;  // values: the ESC (stage3.cu)
   switch (tier) {
     case T_W64: SG_W(6)
     case T_W128: SG_W(7)
