@@ -583,9 +583,10 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
         const int inc = warp_incl_scan(pc, lane);
         int p = nnz + inc - pc;
         if (FILL) sh_st_u16(pre + 2u * (slot * 32u + lane), (unsigned)p);
-        const int cb = lo + ((s0 + b) * 32 + lane) * 32;
+        const int cb = lo + ((s0 + b) * 32 + lane) * 32 - 1;
+        int32_t* q = oc + p;
         while (word) {
-          oc[p++] = cb + __ffs(word) - 1;
+          *q++ = cb + __ffs(word);
           word &= word - 1;
         }
         nnz += __shfl_sync(kFull, inc, 31);
