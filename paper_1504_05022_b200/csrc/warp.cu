@@ -100,11 +100,19 @@ constexpr int kGroup = 4;  // b_j* whose loads are in flight together
 
 // Walk all products of row i in Algorithm-1 order, calling op(c, v, at, act) once per b_j*
 // segment of up to 32 entries (c: this lane's column, v: b_jk, at: a_ij).
+// avs (VALS only, optional): a 32-double shared buffer of the warp; a_ij is then broadcast from
+// it (one LDS.64) instead of two shuffles per b_j*.
 template <bool VALS, typename IT, typename Op>
-__device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_t a1, int lane, Op&& op) {
+__device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_t a1, int lane, Op&& op,
+                                         unsigned avs = 0u) {
   for (int64_t e0 = a0; e0 < a1; e0 += 32) {
     const AChunk<IT> ch = load_achunk<VALS, IT>(a, e0 + lane, a1);
     const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+    if (VALS && avs) {
+      __syncwarp();
+      asm volatile("st.shared.f64 [%0], %1;" ::"r"(avs + 8u * lane), "d"(ch.av) : "memory");
+      __syncwarp();
+    }
     if (!__any_sync(kFull, ch.len > 32)) {
       for (int t0 = 0; t0 < nE; t0 += kGroup) {
         int c[kGroup];
@@ -118,7 +126,11 @@ __device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_
           act[u] = lane < len;
           c[u] = act[u] ? __ldg(a.B.ci + q) : kEmptyKey;
           if (VALS) {
-            at[u] = __shfl_sync(kFull, ch.av, t);
+            if (avs) {
+              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(at[u]) : "r"(avs + 8u * t) : "memory");
+            } else {
+              at[u] = __shfl_sync(kFull, ch.av, t);
+            }
             v[u] = act[u] ? __ldg(a.B.val + q) : 0.0;
           }
         }
@@ -275,6 +287,7 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
     L.o_pre = off;                               // (end of the zeroed region)
     L.o_vals = off;
     off += 8u * (L.nv + 1);  // + scratch
+    off += 256u;             // a_ij of the current chunk (walk_row's avs)
   } else {
     const bool fill = mode == MODE_FILL;
     off = 4u * L.nwd;
@@ -456,6 +469,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     // Lanes of one b_j* hold distinct columns, so no two lanes of an instruction share a slot;
     // successive b_j* are ordered by the warp's in-order shared-memory accesses.
     const unsigned scratch = vals + 8u * unsigned(L.nv);
+    const unsigned avs = MODE == MODE_DENSE ? scratch + 8u : 0u;
     walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       unsigned word, base;
@@ -472,7 +486,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
       sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
-    });
+    }, avs);
     __syncwarp();
     double* ov = a.out_val + o;
     for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
