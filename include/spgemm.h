@@ -139,6 +139,19 @@ spgemm_status_t spgemm_debug_get_u(spgemm_handle_t handle, int64_t* u, int32_t* 
 spgemm_status_t spgemm_set_debug(int32_t force_tier, int64_t long_initial_capacity,
                                  int64_t long_threshold);
 
+/* Testing knob (process-global, next launch): the long-row bitmap kernels process a row's
+ * column window in tiles of at most `tile_columns` columns (rounded up to the kernel's
+ * multiple of 32-column words); 0 = the default, sized by shared memory (1 Mi columns for
+ * counting, 256 Ki for values).  Small values force the multi-tile path on small inputs.
+ * Errors: INVALID_VALUE (negative). */
+spgemm_status_t spgemm_set_debug_long_tile(int64_t tile_columns);
+
+/* Workspace comes from a library-owned stream-ordered memory pool per device that keeps
+ * freed blocks cached (warm multiplies make no OS allocations; the device's default pool and
+ * PyTorch's allocator are not touched).  This returns cached bytes above keep_bytes to the
+ * device (current device; synchronises it).  Errors: CUDA. */
+spgemm_status_t spgemm_trim_workspace_cache(int64_t keep_bytes);
+
 const char* spgemm_status_string(spgemm_status_t s);
 /* Last error text of `handle` (NULL → this thread's last error). */
 const char* spgemm_last_error(spgemm_handle_t handle);

@@ -95,6 +95,10 @@ def load():
     lib.spgemm_debug_get_u.argtypes = [H, P, P]
     lib.spgemm_set_debug.restype = st
     lib.spgemm_set_debug.argtypes = [ctypes.c_int32, I64, I64]
+    lib.spgemm_set_debug_long_tile.restype = st
+    lib.spgemm_set_debug_long_tile.argtypes = [I64]
+    lib.spgemm_trim_workspace_cache.restype = st
+    lib.spgemm_trim_workspace_cache.argtypes = [I64]
     lib.spgemm_status_string.restype = ctypes.c_char_p
     lib.spgemm_status_string.argtypes = [st]
     lib.spgemm_last_error.restype = ctypes.c_char_p

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -49,22 +50,6 @@ __global__ void k_long_slots(const LongState* st, int64_t n, int64_t* slots) {
   if (i < n) slots[i] = long_table_slots(st[i].cap);
 }
 
-// PRECISE numeric: exact long-row tables (cap = nnz(c_i*) from the symbolic pass).
-__global__ void k_long_exact(LongState* st, const int32_t* perm, int64_t first, int64_t n,
-                             const int64_t* nnz_row, const int64_t* arp, int64_t* slots) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int row = perm[first + i];
-  int64_t c = nnz_row[row];
-  if (c < 1) c = 1;
-  st[i].cap = c;
-  st[i].capmax = c;
-  st[i].count = 0;
-  st[i].next_a = arp[row];
-  st[i].done = 0;
-  slots[i] = long_table_slots(c);
-}
-
 __global__ void k_class_sums(int64_t m, const uint8_t* __restrict__ tier, const int64_t* __restrict__ U,
                              const int64_t* __restrict__ arp, const int64_t* __restrict__ nnz_row,
                              unsigned long long* out) {
@@ -82,7 +67,37 @@ __global__ void k_class_sums(int64_t m, const uint8_t* __restrict__ tier, const 
     if (s[i]) atomicAdd(&out[i], s[i]);
 }
 
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t library_pool(int dev) {
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = p;
+  }
+  return g_pools[dev];
+}
+
 }  // namespace
+
+namespace sg {
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = library_pool(dev);
+  if (!pool) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+}  // namespace sg
 
 spgemm_status_t sg_dist_destroy(spgemm_handle_t h);
 bool sg_is_dist(spgemm_handle_t h);
@@ -169,8 +184,8 @@ template <typename T>
 spgemm_status_t dalloc(spgemm_handle_t h, T** p, int64_t count) {
   const size_t bytes = sizeof(T) * size_t(count > 0 ? count : 1);
   void* q = nullptr;
-  cudaError_t e = cudaMallocAsync(&q, bytes, h->stream);
-  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMallocAsync");
+  cudaError_t e = pool_malloc(&q, bytes, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMallocFromPoolAsync");
   h->allocs.emplace_back(q, bytes);
   h->bytes += bytes;
   *p = static_cast<T*>(q);
@@ -320,33 +335,48 @@ spgemm_status_t run_long(spgemm_handle_t h, int mode) {
   return SPGEMM_SUCCESS;
 }
 
-// PRECISE numeric: exact tables (cap = nnz(c_i*)) for the rows of the numeric long class.
-spgemm_status_t prepare_long_exact(spgemm_handle_t h) {
+__global__ void k_gather_long_nnz(const int32_t* __restrict__ perm, int64_t first, int64_t nlong,
+                                  const int64_t* __restrict__ nnz_row, int64_t* __restrict__ out) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nlong) out[k] = nnz_row[perm[first + k]];
+}
+
+// Hybrid long rows after the progressive structure pass: an arena of exactly nnz(c_i*)
+// entries per long row (columns + values), then the rank kernel writes each row there in
+// order with values accumulated in the oracle's order (longbm.cu).
+spgemm_status_t long_values_hybrid(spgemm_handle_t h) {
   const int64_t nl = h->nlong;
-  AL(h, &h->lst, nl);
-  AL(h, &h->lkeys, nl);
-  AL(h, &h->lvals, nl);
-  AL(h, &h->lold_keys, nl);
-  AL(h, &h->lold_vals, nl);
-  AL(h, &h->lold_slots, nl);
-  AL(h, &h->lovf, nl);
-  AL(h, &h->liota, nl);
-  AL(h, &h->lovf_cnt, 1);
-  AL(h, &h->lslots, nl);
-  AL(h, &h->lslot_off, nl + 1);
-  CK(h, cudaMemsetAsync(h->lkeys, 0, sizeof(int32_t*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lvals, 0, sizeof(double*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_vals, 0, sizeof(double*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_slots, 0, sizeof(int64_t) * nl, h->stream));
   const unsigned g = (unsigned)((nl + 255) / 256);
-  k_iota<<<g, 256, 0, h->stream>>>(h->liota, nl);
-  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, 1, h->A, h->B, h->stream));
-  k_long_exact<<<g, 256, 0, h->stream>>>(h->lst, h->ws.perm, h->long_first, nl, h->nnz_row, h->A.rp,
-                                         h->lslots);
+  k_gather_long_nnz<<<g, 256, 0, h->stream>>>(h->ws.perm, h->long_first, nl, h->nnz_row, h->lslots);
   CK(h, cudaGetLastError());
-  h->long_entries = 0;
-  return long_alloc_tables(h, h->liota, nl, true, false);
+  CK(h, launch_exclusive_scan(h->lslots, h->lslot_off, nl, h->scan_tmp, h->stream));
+  CK(h, cudaMemcpyAsync(h->pinned, h->lslot_off + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  spgemm_status_t s = sync(h);
+  if (s != SPGEMM_SUCCESS) return s;
+  const int64_t total = h->pinned[0];
+  int32_t* kb = nullptr;
+  double* vb = nullptr;
+  AL(h, &kb, total);
+  AL(h, &vb, total);
+  h->long_entries = total;
+  CK(h, launch_long_assign(h->liota, nl, h->lslot_off, kb, vb, h->lkeys, h->lvals, nullptr, nullptr,
+                           h->lold_slots, h->lst, h->stream));
+  Stage3Args a{};
+  a.A = h->A;
+  a.B = h->B;
+  a.b_nnz = h->b_nnz;
+  a.n = h->n;
+  a.perm = h->ws.perm;
+  a.first = h->long_first;
+  a.count = nl;
+  a.mode = MODE_FILL;
+  a.bwin = h->ws.bwin;
+  a.row_col = h->lkeys;
+  a.row_val = h->lvals;
+  AL(h, &h->work_ctr, 1);
+  a.work_ctr = h->work_ctr;
+  CK(h, launch_long_bitmap(a, h->stream));
+  return SPGEMM_SUCCESS;
 }
 
 }  // namespace
@@ -390,6 +420,12 @@ spgemm_status_t spgemm_set_debug(int32_t force_tier, int64_t long_initial_capaci
   return SPGEMM_SUCCESS;
 }
 
+spgemm_status_t spgemm_set_debug_long_tile(int64_t tile_columns) {
+  if (tile_columns < 0) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "negative tile width");
+  g_long_tile_words = (tile_columns + 31) / 32;
+  return SPGEMM_SUCCESS;
+}
+
 spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int64_t n,
                               const int64_t* a_row_ptr, const int32_t* a_col_idx,
                               const double* a_val, int64_t a_nnz, const int64_t* b_row_ptr,
@@ -419,16 +455,6 @@ spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int
   h->b_nnz = b_nnz;
   h->A = CsrView{a_row_ptr, a_col_idx, a_val};
   h->B = CsrView{b_row_ptr, b_col_idx, b_val};
-  // keep freed workspace cached in the stream-ordered pool (warm allocations); once per device
-  static thread_local uint64_t pool_done = 0;
-  if (h->device < 64 && !(pool_done & (1ull << h->device))) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_done |= 1ull << h->device;
-  }
   cudaError_t e = cudaSuccess;
   if (!t_pinned) {
     e = cudaMallocHost(&t_pinned, sizeof(int64_t) * (kSumLen + 8));
@@ -458,7 +484,7 @@ spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int
   h->ev_ok = true;
   if (flags & SPGEMM_FLAG_VALIDATE) {
     int32_t* err = nullptr;
-    e = cudaMallocAsync(&err, sizeof(int32_t) * 2, h->stream);
+    e = pool_malloc(reinterpret_cast<void**>(&err), sizeof(int32_t) * 2, h->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int32_t) * 2, h->stream);
     if (e == cudaSuccess) e = launch_validate(m, k, a_row_ptr, a_col_idx, a_nnz, err, h->stream);
     if (e == cudaSuccess) e = launch_validate(k, n, b_row_ptr, b_col_idx, b_nnz, err + 1, h->stream);
@@ -523,9 +549,10 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = false;
   // C~ offsets in both strategies: hybrid keeps whole rows there, precise only the sorted
-  // column sets of the warp classes (4 B/entry) for its numeric pass
-  CK(h, launch_stage1(m, h->k, h->n, h->A, h->B, tp, true, ws, h->stream));
-  CK(h, launch_stage2(m, ws, true, h->n, h->stream));
+  // column sets of the window-bitmap rows (4 B/entry) for its numeric pass
+  const int cap_mode = precise ? CAP_PRECISE : CAP_HYBRID;
+  CK(h, launch_stage1(m, h->k, h->n, h->A, h->B, tp, cap_mode, ws, h->stream));
+  CK(h, launch_stage2(m, ws, cap_mode, h->n, h->stream));
   h->launches_sym = 3;
   tr("alloc + stage 1-2");
   CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
@@ -542,12 +569,9 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->max_u = h->pinned[kSumUMax];
   h->bw_wmax = h->pinned[kSumWmax];
   h->bw_vmax = h->pinned[kSumVmax];
-  {
-    // precise: C~ holds only the warp classes' sorted column sets (STRUCT)
-    bool need = hybrid;
-    need = need || h->tier_count[T_BW] > 0;
-    AL(h, &h->ctil_col, need ? h->sum_cap : 1);
-  }
+  // precise: C~ holds only the window-bitmap rows' sorted column sets (STRUCT); sum_cap counts
+  // only those rows (ctil_capacity, CAP_PRECISE)
+  AL(h, &h->ctil_col, h->sum_cap > 0 ? h->sum_cap : 1);
   if (hybrid) AL(h, &h->ctil_val, h->sum_cap);
   tr("C~ allocation");
   cudaEventRecord(h->ev[1], h->stream);
@@ -587,10 +611,16 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->long_first = h->tier_off[T_LONG];
   if (h->nlong > 0) cudaEventRecord(h->tev[T_LONG][0], h->stream);
   if (hybrid) {
-    // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297]
-    s = run_long(h, MODE_FILL);
+    // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297] finds
+    // each long row's columns; its values then go, in the oracle's order, into an arena of
+    // exactly nnz(c_i*) entries per row (the row's C~ slice, copied by stage 4)
+    s = run_long(h, MODE_COUNT);
     if (s != SPGEMM_SUCCESS) return s;
-    if (h->nlong > 0) h->launches_sym += 4 + 6 * h->growth_rounds;
+    if (h->nlong > 0) {
+      s = long_values_hybrid(h);
+      if (s != SPGEMM_SUCCESS) return s;
+      h->launches_sym += 4 + 6 * h->growth_rounds + 6;
+    }
   } else if (h->nlong > 0) {
     // precise: structure of long rows from a bitmap over the column window
     Stage3Args a{};
@@ -603,6 +633,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     a.count = h->nlong;
     a.nnz_row = h->nnz_row;
     a.mode = MODE_COUNT;
+    a.bwin = ws.bwin;
     AL(h, &h->work_ctr, 1);
     a.work_ctr = h->work_ctr;
     CK(h, launch_long_bitmap(a, h->stream));
@@ -680,7 +711,6 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;
-    a.b_nnz = h->b_nnz;
         a.n = h->n;
         a.perm = h->ws.perm;
         a.first = h->tier_off[t];
@@ -709,7 +739,6 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;
-    a.b_nnz = h->b_nnz;
         a.n = h->n;
         a.perm = h->ws.perm;
         a.first = h->long_first;
@@ -718,6 +747,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
         a.out_col = c_col_idx;
         a.out_val = c_val;
         a.mode = MODE_FILL;
+        a.bwin = h->ws.bwin;
         a.work_ctr = h->work_ctr;
         cudaEventRecord(h->tev[T_LONG][0], h->stream);
         CK(h, launch_long_bitmap(a, h->stream));
@@ -788,7 +818,7 @@ spgemm_status_t spgemm_get_stats(spgemm_handle_t h, spgemm_stats_t* out) {
     if (h->m > 0) {
       unsigned long long* d = nullptr;
       std::vector<unsigned long long> hs(3 * NUM_TIERS);
-      CK(h, cudaMallocAsync(&d, sizeof(unsigned long long) * 3 * NUM_TIERS, h->stream));
+      CK(h, pool_malloc(reinterpret_cast<void**>(&d), sizeof(unsigned long long) * 3 * NUM_TIERS, h->stream));
       CK(h, cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 3 * NUM_TIERS, h->stream));
       k_class_sums<<<256, 256, 0, h->stream>>>(h->m, h->ws.tier, h->ws.U, h->A.rp, h->nnz_row, d);
       CK(h, cudaGetLastError());
@@ -815,6 +845,17 @@ spgemm_status_t spgemm_debug_get_u(spgemm_handle_t h, int64_t* u, int32_t* tier)
     k_tier_to_i32<<<(unsigned)((h->m + 255) / 256), 256, 0, h->stream>>>(h->ws.tier, tier, h->m);
     CK(h, cudaGetLastError());
   }
+  return SPGEMM_SUCCESS;
+}
+
+spgemm_status_t spgemm_trim_workspace_cache(int64_t keep_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = library_pool(dev);
+  if (!pool) return fail(nullptr, SPGEMM_ERROR_CUDA, "no library memory pool");
+  cudaDeviceSynchronize();
+  cudaError_t e = cudaMemPoolTrimTo(pool, keep_bytes > 0 ? (size_t)keep_bytes : 0);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMemPoolTrimTo");
   return SPGEMM_SUCCESS;
 }
 

@@ -61,7 +61,7 @@ __host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap, i
   if (t >= T_G1 && t <= T_G32) return u <= (int64_t(1) << (t - T_G1));
   if (t >= T_W64 && t <= T_W2048) {
     int64_t S = int64_t(64) << (t - T_W64);
-    return 4 * S >= 5 * cap;
+    return 4 * S >= 5 * cap && u <= S;  // table load <= 0.8; the values' ESC holds >= S items
   }
   if (t >= T_C2048 && t <= T_C8192) return cap <= (int64_t(2048) << (t - T_C2048));
   if (t >= T_E2048 && t <= T_E8192) return u <= (int64_t(2048) << (t - T_E2048));
@@ -131,7 +131,7 @@ __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_cl
   }
   if (has_struct)
     for (int t = T_W64; t <= T_W2048; ++t)
-      if ((int64_t(64) << (t - T_W64)) >= 2 * nnz) return t;
+      if ((int64_t(64) << (t - T_W64)) >= 2 * nnz && u <= (int64_t(64) << (t - T_W64))) return t;
   const int e = esc_class(u);
   if (e >= 0) return e;
   for (int t = T_C2048; t <= T_C8192; ++t)
@@ -144,6 +144,15 @@ __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_cl
 __host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n) {
   if (t == T_LONG) return 0;
   return u < n ? u : n;
+}
+// C~ capacity by strategy: CAP_HYBRID keeps whole rows (columns + values) in C~; CAP_PRECISE
+// keeps only the sorted column sets of the window-bitmap rows (STRUCT -> DENSE), no other row
+// needs C~ in the precise strategy.
+enum CapMode : int { CAP_NONE = 0, CAP_HYBRID = 1, CAP_PRECISE = 2 };
+__host__ __device__ inline int64_t ctil_capacity(int mode, int t, int64_t u, int64_t n) {
+  if (mode == CAP_HYBRID) return hybrid_capacity(t, u, n);
+  if (mode == CAP_PRECISE && t == T_BW) return u < n ? u : n;
+  return 0;
 }
 
 struct CsrView {
@@ -181,7 +190,11 @@ struct Stage3Args {
   int32_t* bw_ovf_cnt;        //   (re-run over the full-window bitmap; device counter)
   const int32_t* count_dev;   // if set, the kernel reads its row count here (rows = perm[0..))
   int* work_ctr;              // long rows: dynamic row counter (zeroed by the launcher)
+  int32_t* const* row_col;    // bitmap FILL: per work index r, the row's output columns
+  double* const* row_val;     //   and values (hybrid long-row arena); NULL: out_* at out_off
 };
+// Long-row bitmap tile width in 32-column words (spgemm_set_debug_long_tile; 0 = default).
+extern int64_t g_long_tile_words;
 
 // ---- host-side launchers (defined in the .cu files) --------------------------------
 struct Stage12Ws {
@@ -214,8 +227,8 @@ constexpr int kSumBmax = kSumU + 5;              // max nonzero 1024-column bloc
 constexpr int kSumLen = kSumU + 6;
 
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
-                          bool hybrid_caps, Stage12Ws& ws, cudaStream_t s);
-cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n, cudaStream_t s);
+                          int cap_mode, Stage12Ws& ws, cudaStream_t s);
+cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, cudaStream_t s);
 // PRECISE: re-bin rows by (u_i, nnz(c_i*)) into ws.tier/perm (ws.U and nnz_row are inputs).
 cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParams tp, Stage12Ws& ws,
                          cudaStream_t s);
@@ -303,6 +316,11 @@ struct CopyArgs {
   double* c_val;
 };
 cudaError_t launch_copy(const CopyArgs& a, int group, cudaStream_t s);
+
+// Library-owned stream-ordered pool (one per device, release threshold: keep everything, so
+// warm multiplies allocate without OS calls).  The default device pool is left untouched;
+// spgemm_trim_workspace_cache() returns the cached bytes.
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s);
 
 cudaError_t launch_validate(int64_t rows, int64_t cols, const int64_t* rp, const int32_t* ci,
                             int64_t nnz, int32_t* err, cudaStream_t s);

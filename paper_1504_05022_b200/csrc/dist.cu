@@ -125,7 +125,7 @@ spgemm_status_t dfail(spgemm_dist_s* d, spgemm_status_t s, const std::string& ms
 template <typename T>
 spgemm_status_t dmalloc(spgemm_dist_s* d, T** p, int64_t count) {
   void* q = nullptr;
-  DCK(d, cudaMallocAsync(&q, sizeof(T) * size_t(count > 0 ? count : 1), d->stream));
+  DCK(d, pool_malloc(&q, sizeof(T) * size_t(count > 0 ? count : 1), d->stream));
   d->mem.push_back(q);
   *p = static_cast<T*>(q);
   return SPGEMM_SUCCESS;

@@ -1,17 +1,26 @@
-// longbm.cu — PRECISE strategy, long rows: a bitmap over the row's column window.
+// longbm.cu — rows too long for one shared-memory class (the paper's group 5, [P:222],
+// [P:286-297]) and, for values, the CTA-hash classes: a bitmap over the row's column window.
 //
-// The precise method ([P:165]) first computes the structure, then the values.  For rows too
-// long for a shared-memory hash (the paper's group 5, [P:222]) the structure of row i is
-// the set of columns hit by its products: one bit per column of the window [lo, hi] in
-// shared memory, processed in tiles of kTileBits columns.
-//   k_long_bm_count : per tile, set the bits of all products' columns (atomicOr), count them.
-//                     nnz(c_i*) = total popcount.  No hashing, no probing, no ordering.
-//   k_long_bm_fill  : per tile, rebuild the bits, exclusive prefix popcount per 32-bit word
-//                     → rank(c) = prefix[w] + popc(bits[w] & below(c)) is c's position in the
-//                     sorted row; write C's columns in order, zero the values, then add every
-//                     product into C.val[row_start + rank] (global fp64 atomics, order not
-//                     fixed: checked with the 1e-12·Σ|a||b| tolerance, R1).
+// The precise method ([P:165]) first computes the structure, then the values.  The structure
+// of row i is the set of columns hit by its products: one bit per column of the window
+// [lo, hi] in shared memory, processed in tiles of at most `tile words` x 32 columns.
+//   k_long_bm_count : per tile, set the bits of all products' columns (red.shared.or), count
+//                     them.  nnz(c_i*) = total popcount.  No hashing, no probing, no ordering.
+//   k_long_rank     : per tile, rebuild the bits, exclusive prefix popcount per 32-bit word
+//                     -> rank(c) = prefix[w] + popc(bits[w] & below(c)) is c's position in
+//                     the sorted row; write the row's columns in order.  Values (lines 6, 9,
+//                     11 of Algorithm 1): the tile's ranks are split into NW equal ranges, one
+//                     per warp; every warp walks the row's a_ij in j-ascending order and, of
+//                     each b_j*, only the segment whose columns fall in its range (found by
+//                     binary search: b_j* is sorted), adding a_ij*b_jk into its own ranks of
+//                     the output in place.  Each column is therefore accumulated by one warp,
+//                     in j-ascending order, starting from -0.0 (the identity of +): the
+//                     oracle's order, bit for bit, with no atomics (R1, reading Q1).
+// Tiles exist only because shared memory is finite (c3a: n = 4 Mi columns); a row whose
+// window spans several tiles restricts every b_j* to the tile's columns by binary search
+// too, so each tile visits only its own products (plus one search per a_ij).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -19,10 +28,12 @@ namespace sg {
 
 namespace {
 
-constexpr int kBmNT = 512;
-constexpr int kTileWords = 32768;                 // 1 Mi columns per tile (192 KB with prefix)
+constexpr int kBmNT = 512;                        // count kernel
+constexpr int kRkNT = 256;                        // rank kernel
+constexpr int kRkNW = kRkNT / 32;
+constexpr int kDefaultCountTileWords = 32768;     // 1 Mi columns (128 KB)
+constexpr int kDefaultRankTileWords = 8192;       // 256 Ki columns (64 KB bits + 32 KB ranks)
 constexpr int kChunk = 256;                       // products per work item (load balance)
-constexpr int64_t kTileBits = int64_t(kTileWords) * 32;
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
@@ -53,18 +64,17 @@ __device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
   return ex;
 }
 
-// the row's column window: first / last column of every b_j*
+// the row's column window: first / last column of every b_j* (the (first, last) record of
+// stage 1, a.bwin)
+template <int NT>
 __device__ __forceinline__ void row_window(const Stage3Args& a, int64_t a0, int64_t a1, int* s_red,
                                            int& lo, int& hi) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int l = INT_MAX, h = -1;
-  for (int64_t e = a0 + threadIdx.x; e < a1; e += blockDim.x) {
-    const int j = __ldg(a.A.ci + e);
-    const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
-    if (be > bs) {
-      l = min(l, __ldg(a.B.ci + bs));
-      h = max(h, __ldg(a.B.ci + be - 1));
-    }
+  for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
+    const int4 bw = __ldg(a.bwin + __ldg(a.A.ci + e));
+    l = min(l, bw.x);
+    h = max(h, bw.y);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -78,59 +88,80 @@ __device__ __forceinline__ void row_window(const Stage3Args& a, int64_t a0, int6
   __syncthreads();
   lo = INT_MAX;
   hi = -1;
-  for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
+  for (int k = 0; k < NT / 32; ++k) {
     lo = min(lo, s_red[2 * k]);
     hi = max(hi, s_red[2 * k + 1]);
   }
   __syncthreads();
 }
 
-// Visit every product of row [a0, a1) with a balanced schedule: a_ij are taken NT at a time,
-// each b_j* is cut into kChunk-product work items, and warps take work items round-robin
-// (hub rows of B no longer leave the other warps of the CTA waiting at the barrier).
-struct BmBatch {
-  long long bs[kBmNT];
-  int len[kBmNT];
-  int cinc[kBmNT];  // inclusive scan of work items per a_ij
-  double av[kBmNT];
+// first position q in b_j* = B.ci[bs, bs+len) with B.ci[q] >= c (first/last: b_j*'s range)
+__device__ __forceinline__ int lower_bound_row(const int32_t* __restrict__ bci, int64_t bs, int len, int first,
+                                               int last, int64_t c) {
+  if (c <= first) return 0;
+  if (c > last) return len;
+  int lo = 0, hi = len;  // bci[bs+lo-1] < c <= bci[bs+hi]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(bci + bs + mid) < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// A batch of up to NT a_ij of the row, staged in shared memory, with each b_j*'s segment
+// [s0, s1) restricted to the current tile and its cut into kChunk-product work items.
+template <int NT>
+struct Batch {
+  long long bs[NT];
+  int len[NT];
+  int s0[NT];
+  int cinc[NT];  // inclusive scan of work items per a_ij
+  double av[NT];
 };
 
-template <bool VALS, typename F>
-__device__ __forceinline__ void for_each_product(const Stage3Args& a, int64_t a0, int64_t a1, BmBatch& sb,
-                                                 int* s_w, F&& f) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = kBmNT / 32;
-  for (int64_t e0 = a0; e0 < a1; e0 += kBmNT) {
-    const int64_t e = e0 + threadIdx.x;
-    int len = 0;
-    if (e < a1) {
-      const int j = __ldg(a.A.ci + e);
-      const int64_t bs = __ldg(a.B.rp + j);
-      len = (int)(__ldg(a.B.rp + j + 1) - bs);
-      sb.bs[threadIdx.x] = bs;
-      sb.len[threadIdx.x] = len;
-      if (VALS) sb.av[threadIdx.x] = __ldg(a.A.val + e);
+// Stage the batch [e0, e0+NT) (thread t <-> a_ij t) restricted to columns [cbeg, cend).
+template <int NT, bool VALS>
+__device__ __forceinline__ int stage_batch(const Stage3Args& a, int64_t e0, int64_t a1, int64_t cbeg, int64_t cend,
+                                           bool restrict_cols, Batch<NT>& sb, int* s_w) {
+  const int64_t e = e0 + threadIdx.x;
+  int s0 = 0, s1 = 0;
+  if (e < a1) {
+    const int j = __ldg(a.A.ci + e);
+    const int4 bw = __ldg(a.bwin + j);
+    const int64_t bs = __ldg(a.B.rp + j);
+    const int len = bw.z;
+    s1 = len;
+    if (restrict_cols && len > 0) {
+      s0 = lower_bound_row(a.B.ci, bs, len, bw.x, bw.y, cbeg);
+      s1 = lower_bound_row(a.B.ci, bs, len, bw.x, bw.y, cend);
     }
-    const int nch = (len + kChunk - 1) / kChunk;
-    int tot;
-    const int ex = block_excl_scan_i<kBmNT>(nch, &tot, s_w);
-    sb.cinc[threadIdx.x] = ex + nch;
-    __syncthreads();
-    for (int item = w; item < tot; item += NW) {
-      int lo = 0, hi = kBmNT - 1;  // first t with cinc[t] > item
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sb.cinc[mid] > item) hi = mid;
-        else lo = mid + 1;
-      }
-      const int t = lo;
-      const int first_item = sb.cinc[t] - (sb.len[t] + kChunk - 1) / kChunk;
-      const int64_t q0 = sb.bs[t] + int64_t(item - first_item) * kChunk;
-      const int64_t qe = min(q0 + kChunk, (int64_t)sb.bs[t] + sb.len[t]);
-      const double at = VALS ? sb.av[t] : 0.0;
-      for (int64_t q = q0 + lane; q < qe; q += 32) f(q, at);
-    }
-    __syncthreads();
+    sb.bs[threadIdx.x] = bs;
+    sb.len[threadIdx.x] = s1;
+    sb.s0[threadIdx.x] = s0;
+    if (VALS) sb.av[threadIdx.x] = __ldg(a.A.val + e);
   }
+  const int nch = (s1 - s0 + kChunk - 1) / kChunk;
+  int tot;
+  const int ex = block_excl_scan_i<NT>(nch, &tot, s_w);
+  sb.cinc[threadIdx.x] = ex + nch;
+  __syncthreads();
+  return tot;
+}
+
+// Work item -> (a_ij slot t, product range [q0, qe) of b_j*), balanced over warps.
+template <int NT>
+__device__ __forceinline__ void work_item(const Batch<NT>& sb, int item, int& t, int64_t& q0, int64_t& qe) {
+  int lo = 0, hi = NT - 1;  // first t with cinc[t] > item
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sb.cinc[mid] > item) hi = mid;
+    else lo = mid + 1;
+  }
+  t = lo;
+  const int first_item = sb.cinc[t] - (sb.len[t] - sb.s0[t] + kChunk - 1) / kChunk;
+  q0 = sb.bs[t] + sb.s0[t] + int64_t(item - first_item) * kChunk;
+  qe = min(q0 + kChunk, (int64_t)sb.bs[t] + sb.len[t]);
 }
 
 // Long rows differ by orders of magnitude in work (c3b: 8 Ki to 2.5 Mi products): CTAs take
@@ -143,38 +174,58 @@ __device__ __forceinline__ int64_t next_row(const Stage3Args& a, int64_t r, int6
   return *s_next;
 }
 
-__global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
+__device__ __forceinline__ void sh_red_or(unsigned* p, unsigned v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+// Words of a tile: the row's window in multiples of NT words, at most tmax.
+template <int NT>
+__device__ __forceinline__ int tile_words(int lo, int hi, int64_t tmax) {
+  const int64_t wwords = (int64_t(hi) - lo) / 32 + 1;
+  const int64_t t = wwords < tmax ? wwords : tmax;
+  return (int)((t + NT - 1) / NT * NT);
+}
+
+// ------------------------------------------------------------------------- count (symbolic)
+__global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
   __shared__ int s_red[2 * (kBmNT / 32)];
   __shared__ int s_w[kBmNT / 32 + 1];
-  __shared__ BmBatch sb;
+  __shared__ Batch<kBmNT> sb;
   __shared__ unsigned long long s_cnt;
   __shared__ int64_t s_next;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int lo, hi;
-    row_window(a, a0, a1, s_red, lo, hi);
+    row_window<kBmNT>(a, a0, a1, s_red, lo, hi);
     if (threadIdx.x == 0) s_cnt = 0;
-    // tile: the row's window, at most kTileBits columns, in multiples of kBmNT words
-    const int64_t wwords = (int64_t(hi) - lo) / 32 + 1;
-    const int64_t tmax = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
-                             ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
-    const int tw = (int)((wwords < tmax ? wwords : tmax) + kBmNT - 1) / kBmNT * kBmNT;
+    const int tw = tile_words<kBmNT>(lo, hi, tmax);
     const int64_t tbits = int64_t(tw) * 32;
+    const bool multi = int64_t(hi) - lo + 1 > tbits;
     for (int64_t base = lo; base <= hi; base += tbits) {
       for (int k = threadIdx.x; k < tw; k += kBmNT) bm[k] = 0u;
       __syncthreads();
-      for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
-        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < tbits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
-      });
+      for (int64_t e0 = a0; e0 < a1; e0 += kBmNT) {
+        const int items = stage_batch<kBmNT, false>(a, e0, a1, base, base + tbits, multi, sb, s_w);
+        for (int item = w; item < items; item += kBmNT / 32) {
+          int t;
+          int64_t q0, qe;
+          work_item<kBmNT>(sb, item, t, q0, qe);
+          for (int64_t q = q0 + lane; q < qe; q += 32) {
+            const unsigned d = (unsigned)(__ldg(a.B.ci + q) - base);  // in [0, tbits): restricted
+            sh_red_or(&bm[d >> 5], 1u << (d & 31));                    // line 8: insert
+          }
+        }
+        __syncthreads();
+      }
       unsigned c = 0;
       for (int k = threadIdx.x; k < tw; k += kBmNT) c += __popc(bm[k]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, (unsigned long long)c);
+      if (lane == 0) atomicAdd(&s_cnt, (unsigned long long)c);
       __syncthreads();
     }
     if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = (int64_t)s_cnt;
@@ -182,72 +233,151 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a) {
   }
 }
 
-__global__ void __launch_bounds__(kBmNT) k_long_bm_fill(Stage3Args a) {
+// --------------------------------------------------------------------- rank fill (values)
+// Output of work index r (position in the class): C's row at out_off[row] (precise, C~
+// classes) or the per-row arena pointers row_col[r] / row_val[r] (hybrid long rows).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
-  const int64_t tmax0 = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
-                            ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
-  int* pre = reinterpret_cast<int*>(smem + size_t(tmax0) * sizeof(unsigned));
-  __shared__ int s_red[2 * (kBmNT / 32)];
-  __shared__ int s_w[kBmNT / 32 + 1];
-  __shared__ BmBatch sb;
+  int* pre = reinterpret_cast<int*>(smem + size_t(tmax) * sizeof(unsigned));
+  __shared__ int s_red[2 * NW];
+  __shared__ int s_w[NW + 1];
+  __shared__ Batch<NT> sb;
+  __shared__ int s_split[NT][NW + 1];
+  __shared__ int s_cb[NW + 1];
   __shared__ int64_t s_next;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    const int64_t o = __ldg(a.out_off + row);
+    int32_t* oc;
+    double* ov;
+    if (a.row_col) {
+      oc = a.row_col[r];
+      ov = a.row_val[r];
+    } else {
+      const int64_t o = __ldg(a.out_off + row);
+      oc = a.out_col + o;
+      ov = a.out_val + o;
+    }
     int lo, hi;
-    row_window(a, a0, a1, s_red, lo, hi);
-    const int64_t wwords = (int64_t(hi) - lo) / 32 + 1;
-    const int64_t tmax = (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) < kTileWords
-                             ? (((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT) : kTileWords;
-    const int tw = (int)((wwords < tmax ? wwords : tmax) + kBmNT - 1) / kBmNT * kBmNT;
+    row_window<NT>(a, a0, a1, s_red, lo, hi);
+    const int tw = tile_words<NT>(lo, hi, tmax);
     const int64_t tbits = int64_t(tw) * 32;
-    const int WPT = tw / kBmNT;  // words per thread in the prefix scan
-    int64_t done = 0;  // entries of the row already placed by earlier tiles
+    const bool multi = int64_t(hi) - lo + 1 > tbits;
+    const int WPT = tw / NT;  // words per thread in the prefix scan
+    int64_t done = 0;         // entries of the row placed by earlier tiles
     for (int64_t base = lo; base <= hi; base += tbits) {
-      for (int k = threadIdx.x; k < tw; k += kBmNT) bm[k] = 0u;
+      const int64_t tend = min(base + tbits, int64_t(hi) + 1);
+      for (int k = threadIdx.x; k < tw; k += NT) bm[k] = 0u;
       __syncthreads();
-      for_each_product<false>(a, a0, a1, sb, s_w, [&](int64_t q, double) {
-        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < tbits) atomicOr(&bm[d >> 5], 1u << (d & 31));  // line 8: insert
-      });
-      // exclusive prefix popcount over the tile's words (thread t owns words [t·WPT, +WPT))
+      // 1. the tile's bits (line 8 of Algorithm 1 for every product of the tile)
+      for (int64_t e0 = a0; e0 < a1; e0 += NT) {
+        const int items = stage_batch<NT, false>(a, e0, a1, base, tend, multi, sb, s_w);
+        for (int item = w; item < items; item += NW) {
+          int t;
+          int64_t q0, qe;
+          work_item<NT>(sb, item, t, q0, qe);
+          for (int64_t q = q0 + lane; q < qe; q += 32) {
+            const unsigned d = (unsigned)(__ldg(a.B.ci + q) - base);
+            sh_red_or(&bm[d >> 5], 1u << (d & 31));
+          }
+        }
+        __syncthreads();
+      }
+      // 2. exclusive prefix popcount per word (thread t owns words [t*WPT, (t+1)*WPT)); the
+      //    tile's columns in order; values start at -0.0 (the identity of +: the first add
+      //    is line 9's assignment)
       int loc = 0;
       for (int k = 0; k < WPT; ++k) loc += __popc(bm[threadIdx.x * WPT + k]);
-      int tot;
-      int run = block_excl_scan_i<kBmNT>(loc, &tot, s_w);
+      int T;
+      int run = block_excl_scan_i<NT>(loc, &T, s_w);
+      const int run0 = run;
       for (int k = 0; k < WPT; ++k) {
         const int wi = threadIdx.x * WPT + k;
-        const unsigned bits = bm[wi];
-        if ((wi & 1) == 0) pre[wi >> 1] = run;
-        // C's columns of this tile, in order, and zeroed values
-        unsigned b = bits;
+        unsigned b = bm[wi];
+        pre[wi] = run;
         int p = run;
+        const int cb = (int)(base + int64_t(wi) * 32);
         while (b) {
-          const int bit = __ffs(b) - 1;
+          oc[done + p] = cb + __ffs(b) - 1;
+          ov[done + p] = -0.0;
           b &= b - 1;
-          a.out_col[o + done + p] = (int)(base + int64_t(wi) * 32 + bit);
-          a.out_val[o + done + p] = 0.0;
           ++p;
         }
-        run += __popc(bits);
+        run = p;
       }
-      __threadfence();
-      __syncthreads();
-      // values: every product of a column in this tile adds into its rank (line 11)
-      for_each_product<true>(a, a0, a1, sb, s_w, [&](int64_t q, double at) {
-        const int64_t d = int64_t(__ldg(a.B.ci + q)) - base;
-        if (d >= 0 && d < tbits) {
-          const int wi = (int)(d >> 5);
-          const unsigned below = (1u << (d & 31)) - 1u;
-          const int rank = pre[wi >> 1] + ((wi & 1) ? __popc(bm[wi - 1]) : 0) + __popc(bm[wi] & below);
-          atomicAdd(a.out_val + o + done + rank, __dmul_rn(at, __ldg(a.B.val + q)));
+      // rank ranges of the warps: warp k owns ranks [floor(k*T/NW), floor((k+1)*T/NW)),
+      // i.e. columns [cb[k], cb[k+1])
+      if (threadIdx.x == 0) {
+        s_cb[0] = (int)base;
+        s_cb[NW] = (int)tend;
+      }
+      for (int k = 1; k < NW; ++k) {
+        const int rk = (int)((int64_t(k) * T) / NW);
+        if (rk >= run0 && rk < run) {  // the word holding rank rk is one of mine
+          int q = run0;
+          for (int kk = 0; kk < WPT; ++kk) {
+            const int wi = threadIdx.x * WPT + kk;
+            unsigned b = bm[wi];
+            const int pc = __popc(b);
+            if (rk < q + pc) {
+              for (int s = rk - q; s > 0; --s) b &= b - 1;  // drop the lower set bits
+              s_cb[k] = (int)(base + int64_t(wi) * 32 + __ffs(b) - 1);
+              break;
+            }
+            q += pc;
+          }
         }
-      });
-      done += tot;
+        if (rk >= T) {
+          if (threadIdx.x == 0) s_cb[k] = (int)tend;
+        }
+      }
+      __syncthreads();
+      // 3. values: warp w walks the a_ij in order, its own column range of each b_j*
+      if (T > 0) {
+        for (int64_t e0 = a0; e0 < a1; e0 += NT) {
+          const int64_t e = e0 + threadIdx.x;
+          if (e < a1) {
+            const int j = __ldg(a.A.ci + e);
+            const int4 bw = __ldg(a.bwin + j);
+            const int64_t bs = __ldg(a.B.rp + j);
+            sb.bs[threadIdx.x] = bs;
+            sb.av[threadIdx.x] = __ldg(a.A.val + e);
+#pragma unroll 1
+            for (int k = 0; k <= NW; ++k)
+              s_split[threadIdx.x][k] = bw.z > 0 ? lower_bound_row(a.B.ci, bs, bw.z, bw.x, bw.y, s_cb[k]) : 0;
+          }
+          __syncthreads();
+          const int na = (int)min(int64_t(NT), a1 - e0);
+          for (int t = 0; t < na; ++t) {
+            const int s = s_split[t][w], en = s_split[t][w + 1];
+            if (s >= en) continue;
+            const int64_t bs = sb.bs[t];
+            const double at = sb.av[t];
+            for (int q0 = s; q0 < en; q0 += 32) {
+              const int q = q0 + lane;
+              if (q < en) {
+                const int c = __ldg(a.B.ci + bs + q);
+                const double v = __ldg(a.B.val + bs + q);
+                const unsigned d = (unsigned)(c - base);
+                const unsigned wd = d >> 5;
+                const int rank = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u));
+                double* p = ov + done + rank;
+                *p = __dadd_rn(*p, __dmul_rn(at, v));  // lines 6, 9, 11: c_ik += a_ij b_jk
+              }
+              __syncwarp();  // the next segment may add into a column this one just wrote
+            }
+          }
+          __syncthreads();
+        }
+      }
+      done += T;
       __syncthreads();
     }
+    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = done;
     __syncthreads();
   }
 }
@@ -259,31 +389,49 @@ int sm_count() {
   return n > 0 ? n : 148;
 }
 
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
 }  // namespace
+
+int64_t g_long_tile_words = 0;  // debug knob (spgemm_set_debug_long_tile): 0 = by shared memory
 
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  const bool fill = a.mode == MODE_FILL;
   if (a.work_ctr) {
     cudaError_t e0 = cudaMemsetAsync(a.work_ctr, 0, sizeof(int), s);
     if (e0 != cudaSuccess) return e0;
   }
-  // tiles never exceed the column range [0, n): size shared memory by it (c3b: 8 Ki words)
-  const int64_t nwords = ((a.n + 31) / 32 + 1 + kBmNT - 1) / kBmNT * kBmNT;
-  const int64_t tw = nwords < kTileWords ? nwords : kTileWords;
-  const size_t sm = size_t(tw) * (fill ? 6 : 4);
-  auto kern = fill ? k_long_bm_fill : k_long_bm_count;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
+  const bool fill = a.mode == MODE_FILL;
+  const int nt = fill ? kRkNT : kBmNT;
+  // tiles never exceed the column range [0, n)
+  const int64_t nwords = round_up((a.n + 31) / 32 + 1, nt);
+  int64_t tmax = fill ? kDefaultRankTileWords : kDefaultCountTileWords;
+  static const int64_t env_tw = getenv("SPGEMM_LONG_TILE_WORDS") ? atoll(getenv("SPGEMM_LONG_TILE_WORDS")) : 0;
+  if (env_tw > 0) tmax = env_tw;
+  if (g_long_tile_words > 0) tmax = g_long_tile_words;
+  tmax = round_up(tmax, nt);
+  if (tmax > nwords) tmax = nwords;
+  const size_t sm = size_t(tmax) * (fill ? 8 : 4);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBmNT, sm);
-  if (per_sm < 1) per_sm = 1;
-  // fill: at most two CTAs per SM keep the rows being accumulated (fp64 atomics into C) plus
-  // B resident in L2; more concurrent rows thrash it (c3b: 1 CTA 88 ms, 2 CTAs 76, 3 CTAs 81)
-  if (fill && per_sm > 2) per_sm = 2;
-  int64_t grid = int64_t(sm_count()) * per_sm;
-  if (grid > a.count) grid = a.count;
-  kern<<<(unsigned)grid, kBmNT, sm, s>>>(a);
+  cudaError_t e;
+  if (fill) {
+    auto kern = k_long_rank<kRkNT>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, sm);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = int64_t(sm_count()) * per_sm;
+    if (grid > a.count) grid = a.count;
+    kern<<<(unsigned)grid, nt, sm, s>>>(a, (int)tmax);
+  } else {
+    e = cudaFuncSetAttribute(k_long_bm_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_bm_count, nt, sm);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = int64_t(sm_count()) * per_sm;
+    if (grid > a.count) grid = a.count;
+    k_long_bm_count<<<(unsigned)grid, nt, sm, s>>>(a, (int)tmax);
+  }
   return cudaGetLastError();
 }
 

@@ -10,8 +10,6 @@
 //                     class: deterministic) + exclusive scan of capacities → C~ offsets
 #include <climits>
 
-#include <cub/warp/warp_reduce.cuh>
-
 #include "common.cuh"
 
 namespace sg {
@@ -80,7 +78,7 @@ template <int NT, int RPT>
 __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
                                                const int64_t* __restrict__ brp,
                                                const int4* __restrict__ bwin, TierParams tp,
-                                               int hybrid, int64_t* __restrict__ U,
+                                               int cap_mode, int64_t* __restrict__ U,
                                                uint8_t* __restrict__ tier, int32_t* __restrict__ rlo,
                                                int32_t* __restrict__ blk_tier,
                                                int64_t* __restrict__ blk_cap,
@@ -116,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
       tier[i] = (uint8_t)t;
       rlo[i] = lo;
       atomicAdd(&s_hist[t], 1);
-      capsum += hybrid ? hybrid_capacity(t, u, n) : 0;
+      capsum += ctil_capacity(cap_mode, t, u, n);
       usum += u;
       umax = u > umax ? u : umax;
       if (t == T_BW) {
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(NT) k_stage2_scan(int64_t nblk, int32_t* blk_t
 }
 
 template <int NT, int RPT>
-__global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int hybrid,
+__global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int cap_mode,
                                                        const uint8_t* __restrict__ tier,
                                                        const int64_t* __restrict__ U,
                                                        const int32_t* __restrict__ blk_tier_off,
@@ -300,7 +298,7 @@ __global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     const bool valid = i < m;
     const int t = valid ? (int)tier[i] : NUM_TIERS;
-    const int64_t cap = (valid && hybrid) ? hybrid_capacity(t, U[i], n) : 0;
+    const int64_t cap = valid ? ctil_capacity(cap_mode, t, U[i], n) : 0;
     const unsigned peers = __match_any_sync(0xffffffffu, t);
     const int wrank = __popc(peers & lanemask_lt());
     if (wrank == 0) s_wcnt[w][t] = __popc(peers);
@@ -310,7 +308,7 @@ __global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int
       int pos = s_run[t] + wrank;
       for (int k = 0; k < w; ++k) pos += s_wcnt[k][t];
       perm[pos] = (int32_t)i;
-      if (hybrid) ctil_off[i] = cap_carry + ex;
+      if (cap_mode != CAP_NONE) ctil_off[i] = cap_carry + ex;
     }
     cap_carry += tot;
     __syncthreads();
@@ -422,24 +420,24 @@ __global__ void k_validate(int64_t rows, int64_t cols, const int64_t* __restrict
 }  // namespace
 
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
-                          bool hybrid_caps, Stage12Ws& ws, cudaStream_t s) {
+                          int cap_mode, Stage12Ws& ws, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 3 * sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   if (k > 0) k_bwin<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, B.rp, B.ci, ws.bwin);
   k_stage1<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, A, B.rp, ws.bwin, tp, hybrid_caps ? 1 : 0, ws.U, ws.tier, ws.rlo, ws.blk_tier, ws.blk_cap,
+      m, n, A, B.rp, ws.bwin, tp, cap_mode, ws.U, ws.tier, ws.rlo, ws.blk_tier, ws.blk_cap,
       ws.blk_usum, ws.blk_umax, ws.summary);
   return cudaGetLastError();
 }
 
-cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, bool hybrid_caps, int64_t n, cudaStream_t s) {
+cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, cudaStream_t s) {
   k_stage2_scan<1024><<<1, 1024, 0, s>>>(ws.nblk, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax,
                                          ws.summary);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || m == 0) return e;
   k_stage2_scatter<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, hybrid_caps ? 1 : 0, ws.tier, ws.U, ws.blk_tier, ws.blk_cap, ws.perm, ws.ctil_off);
+      m, n, cap_mode, ws.tier, ws.U, ws.blk_tier, ws.blk_cap, ws.perm, ws.ctil_off);
   return cudaGetLastError();
 }
 
@@ -452,7 +450,7 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
       m, n, ws.U, nnz_row, tp, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax, ws.summary);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_stage2(m, ws, false, n, s);
+  return launch_stage2(m, ws, CAP_NONE, n, s);
 }
 
 int64_t scan_tmp_elems(int64_t len) { return (len + kScanTile - 1) / kScanTile + 2; }

@@ -10,9 +10,9 @@
 //                sorted by (column, product index) with a register bitonic network and
 //                fused left to right — the ESC idea with the whole row in registers.
 //   (warp.cu)    one warp per row, S-slot shared-memory hash (classes w64..w2048).
-//   k_cta_hash   one CTA per row, order-preserving hash (home slot monotone in the column)
-//                with linear probing into 2H slots: clusters come out ordered, only each
-//                cluster is insertion-sorted before the ordered compaction.
+//   k_cta_hash   one CTA per row, a 2H-slot shared-memory hash that counts the row's
+//                distinct columns (symbolic); the values of these rows come from the ESC
+//                (esc.cu) or the bitmap rank kernel (longbm.cu).
 // Values: products are rounded separately (__dmul_rn, no FMA) and summed with __dadd_rn.
 // k_group and the warp classes add in j-ascending order starting from the first product (the
 // warp hash starts from -0.0, the identity of +), i.e. the oracle's order [P:129-131].
@@ -166,108 +166,35 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
   }
 }
 
-// --------------------------------------------------------------- CTA order-preserving hash
-template <int NT>
-__device__ __forceinline__ int block_excl_scan_int(int v, int* total, int* s_w) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int x = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += x;
-  }
-  if (lane == 31) s_w[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    const int x = lane < NT / 32 ? s_w[lane] : 0;
-    int xi = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, xi, o);
-      if (lane >= o) xi += y;
-    }
-    if (lane < NT / 32) s_w[lane] = xi - x;
-    if (lane == 31) s_w[NT / 32] = xi;
-  }
-  __syncthreads();
-  const int ex = inc - v + s_w[w];
-  *total = s_w[NT / 32];
-  __syncthreads();
-  return ex;
-}
-
+// --------------------------------------------------------------- CTA hash (counting)
+// COUNT only (precise symbolic and the e / c classes): nnz(c_i*) = the number of distinct
+// columns the row's products insert ([P:121-135] lines 7-8 / 10 without values).  The values
+// of these rows come from the ESC (e classes) or the bitmap rank kernel (c classes).
 template <int LOG2H, int NT>
 __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
   constexpr int H = 1 << LOG2H;
-  constexpr int S = 2 * H;       // physical slots (nnz <= H: load <= 1/2)
-  constexpr int SPREAD = S - 64;  // order-preserving homes cover [0, SPREAD)
+  constexpr int S = 2 * H;  // physical slots (nnz <= H: load <= 1/2)
   constexpr int NW = NT / 32;
-  constexpr int kLongCluster = 96;  // longer clusters: whole-row bitonic sort instead
   extern __shared__ __align__(16) unsigned char smem[];
   int* keys = reinterpret_cast<int*>(smem);
-  double* vals = reinterpret_cast<double*>(smem + size_t(S) * sizeof(int));
-  __shared__ int s_w[NW + 1];
-  __shared__ int s_lo[NW], s_hi[NW];
-  __shared__ int s_cnt, s_slow;
+  __shared__ int s_cnt;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const bool fill = a.mode == MODE_FILL;
 
   const int64_t rper = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
   const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, a.count);
   for (int64_t r = int64_t(blockIdx.x) * rper; r < rend; ++r) {
     const int row = __ldg(a.perm + a.first + r);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    // column window [lo, hi] of the row: first/last column of each b_j*
-    int lo = INT_MAX, hi = -1;
-    if (fill) {
-      for (int64_t e = a0 + threadIdx.x; e < a1; e += NT) {
-        const int j = __ldg(a.A.ci + e);
-        const int64_t bs = __ldg(a.B.rp + j), be = __ldg(a.B.rp + j + 1);
-        if (be > bs) {
-          lo = min(lo, __ldg(a.B.ci + bs));
-          hi = max(hi, __ldg(a.B.ci + be - 1));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      if (lane == 0) {
-        s_lo[w] = lo;
-        s_hi[w] = hi;
-      }
-    }
-    for (int s = threadIdx.x; s < S; s += NT) {
-      keys[s] = kEmptyKey;
-      if (fill) vals[s] = 0.0;
-    }
-    if (threadIdx.x == 0) {
-      s_cnt = 0;
-      s_slow = 0;
-    }
+    for (int s = threadIdx.x; s < S; s += NT) keys[s] = kEmptyKey;
+    if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    float scale = 1.0f;
-    if (fill) {
-      lo = s_lo[0];
-      hi = s_hi[0];
-      for (int k = 1; k < NW; ++k) {
-        lo = min(lo, s_lo[k]);
-        hi = max(hi, s_hi[k]);
-      }
-      const int64_t W = int64_t(hi) - lo + 1;
-      scale = W <= SPREAD ? 1.0f : (float)SPREAD / (float)W;
-    }
-    int inserted = 0, wrapped = 0;
+    int inserted = 0;
     for (int64_t e = a0 + w; e < a1; e += NW) {
       const int j = __ldg(a.A.ci + e);
-      const double at = fill ? __ldg(a.A.val + e) : 0.0;
       const int64_t jb = __ldg(a.B.rp + j), je = __ldg(a.B.rp + j + 1);
       for (int64_t q = jb + lane; q < je; q += 32) {
         const int c = __ldg(a.B.ci + q);
-        // FILL: order-preserving home (monotone in c); COUNT: any spread hash
-        int h = fill ? min((int)__fmul_rz((float)(c - lo), scale), SPREAD - 1)
-                     : (int)(((unsigned)c * 0x9E3779B1u) >> (32 - LOG2H - 1));
+        int h = (int)(((unsigned)c * 0x9E3779B1u) >> (32 - LOG2H - 1));
         volatile int* vk = keys;
         while (true) {
           const int k = vk[h];
@@ -280,120 +207,15 @@ __global__ void __launch_bounds__(NT) k_cta_hash(Stage3Args a) {
             }
             if (old == c) break;
           }
-          if (++h == S) {
-            h = 0;
-            wrapped = 1;
-          }
+          h = (h + 1) & (S - 1);
         }
-        if (fill) atomicAdd(&vals[h], __dmul_rn(at, __ldg(a.B.val + q)));
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
-      wrapped |= __shfl_xor_sync(0xffffffffu, wrapped, o);
-    }
-    if (lane == 0) {
-      atomicAdd(&s_cnt, inserted);
-      if (wrapped) s_slow = 1;
-    }
+    for (int o = 16; o > 0; o >>= 1) inserted += __shfl_xor_sync(0xffffffffu, inserted, o);
+    if (lane == 0) atomicAdd(&s_cnt, inserted);
     __syncthreads();
-    const int nnz = s_cnt;
-    if (!fill) {
-      if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = nnz;
-      __syncthreads();
-      continue;
-    }
-    const int64_t o = __ldg(a.out_off + row);
-    if (!s_slow) {
-      // order each cluster (maximal run of occupied slots) by insertion sort; a long
-      // cluster (clustered columns) switches the row to the bitonic path below
-      constexpr int CH = S / NT;
-      for (int s = threadIdx.x * CH; s < (threadIdx.x + 1) * CH; ++s) {
-        if (keys[s] == kEmptyKey || (s > 0 && keys[s - 1] != kEmptyKey)) continue;
-        int end = s + 1;
-        while (end < S && keys[end] != kEmptyKey && end - s <= kLongCluster) ++end;
-        if (end - s > kLongCluster) {
-          s_slow = 1;
-          break;
-        }
-        for (int x = s + 1; x < end; ++x) {
-          const int kx = keys[x];
-          const double vx = vals[x];
-          int y = x - 1;
-          while (y >= s && keys[y] > kx) {
-            keys[y + 1] = keys[y];
-            vals[y + 1] = vals[y];
-            --y;
-          }
-          keys[y + 1] = kx;
-          vals[y + 1] = vx;
-        }
-      }
-      __syncthreads();
-    }
-    if (!s_slow) {
-      // ordered compaction: each thread owns CH consecutive slots; one block scan of counts
-      constexpr int CH = S / NT;
-      const int s0 = threadIdx.x * CH;
-      int cnt = 0;
-#pragma unroll
-      for (int k = 0; k < CH; ++k) cnt += keys[s0 + k] != kEmptyKey;
-      int tot;
-      int pos = block_excl_scan_int<NT>(cnt, &tot, s_w);
-      for (int k = 0; k < CH; ++k) {
-        const int kk = keys[s0 + k];
-        if (kk != kEmptyKey) {
-          a.out_col[o + pos] = kk;
-          a.out_val[o + pos] = vals[s0 + k];
-          ++pos;
-        }
-      }
-    } else {
-      // robust path: compact (key, value) pairs to the front, bitonic sort by key, write
-      int base = 0;
-      for (int s0 = 0; s0 < S; s0 += NT) {
-        const int s = s0 + threadIdx.x;
-        const int k = keys[s];
-        const double v = vals[s];
-        const bool occ = k != kEmptyKey;
-        int tot;
-        const int pos = block_excl_scan_int<NT>(occ ? 1 : 0, &tot, s_w);  // has __syncthreads
-        if (occ) {
-          keys[base + pos] = k;
-          vals[base + pos] = v;
-        }
-        base += tot;
-        __syncthreads();
-      }
-      int N = 1;
-      while (N < nnz) N <<= 1;
-      for (int s = nnz + threadIdx.x; s < N; s += NT) keys[s] = INT_MAX;
-      __syncthreads();
-      for (int kk = 2; kk <= N; kk <<= 1) {
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-          for (int i = threadIdx.x; i < (N >> 1); i += NT) {
-            const int l0 = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-            const int l1 = l0 + j;
-            const bool asc = (l0 & kk) == 0;
-            const int k0 = keys[l0], k1 = keys[l1];
-            if ((k0 > k1) == asc) {
-              keys[l0] = k1;
-              keys[l1] = k0;
-              const double t = vals[l0];
-              vals[l0] = vals[l1];
-              vals[l1] = t;
-            }
-          }
-          __syncthreads();
-        }
-      }
-      for (int t = threadIdx.x; t < nnz; t += NT) {
-        a.out_col[o + t] = keys[t];
-        a.out_val[o + t] = vals[t];
-      }
-    }
-    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = s_cnt;
     __syncthreads();
   }
 }
@@ -438,11 +260,10 @@ cudaError_t launch_persistent(K kernel, int nt, size_t dsmem, int64_t work_units
 
 cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  const bool fill = a.mode == MODE_FILL || a.mode == MODE_DENSE;
-  const size_t per_slot = fill ? 12 : 4;
+  constexpr size_t per_slot = 4;  // k_cta_hash counts only
   switch (tier) {
 #define SG_GROUP(G, UPB)                                                                      \
-  return a.n <= (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true>, 256, 0, a.count, UPB, a, s) \
+  return a.n < (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true>, 256, 0, a.count, UPB, a, s) \
                                    : launch_persistent(k_group<G, 256, false>, 256, 0, a.count, UPB, a, s)
     case T_G1: SG_GROUP(1, 256);
     case T_G2: SG_GROUP(2, 128);
@@ -475,6 +296,15 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
     case T_E8192:
       if (a.mode == MODE_COUNT) return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * 4, a.count, 1, a, s);
       return launch_esc(tier, a, s);
+    // values of the CTA-hash classes: the bitmap rank kernel (longbm.cu) — ordered, no atomics
+    case T_C2048:
+    case T_C4096:
+    case T_C8192:
+      if (a.mode == MODE_FILL) return launch_long_bitmap(a, s);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  switch (tier) {
     case T_C2048: return launch_persistent(k_cta_hash<11, 256>, 256, 4096 * per_slot, a.count, 1, a, s);
     case T_C4096: return launch_persistent(k_cta_hash<12, 512>, 512, 8192 * per_slot, a.count, 1, a, s);
     case T_C8192: return launch_persistent(k_cta_hash<13, 512>, 512, 16384 * per_slot, a.count, 1, a, s);

@@ -72,6 +72,18 @@ def set_debug(force_tier: int = -1, long_initial_capacity: int = 0, long_thresho
     check(lib.spgemm_set_debug(force_tier, long_initial_capacity, long_threshold))
 
 
+def set_debug_long_tile(tile_columns: int = 0):
+    """Testing knob: long-row bitmap tiles of at most tile_columns columns (0 = default)."""
+    lib = load()
+    check(lib.spgemm_set_debug_long_tile(int(tile_columns)))
+
+
+def trim_workspace_cache(keep_bytes: int = 0):
+    """Return the library pool's cached device memory above keep_bytes."""
+    lib = load()
+    check(lib.spgemm_trim_workspace_cache(int(keep_bytes)))
+
+
 def partition_rows(u_inclusive_scan, nranks: int):
     """Host partition rule of dist_symbolic (numpy int64 in, numpy int64 splits out)."""
     import numpy as np

@@ -24,8 +24,10 @@ GOLD = json.load(open(os.path.join(HERE, "golden", "spec_examples.json")))
 def _reset_debug():
     import paper_1504_05022_b200 as sg
     sg.set_debug(-1, 0, 0)
+    sg.set_debug_long_tile(0)
     yield
     sg.set_debug(-1, 0, 0)
+    sg.set_debug_long_tile(0)
 
 
 def _dense_csr(D, pattern=None):
@@ -366,8 +368,7 @@ def _wide_pair(seed, a_lens, n=400_000, k=2000, blen=64):
 @pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
 def test_determinism_real_all_classes(flags_name):
     """Run-to-run bit-identical values in real mode through the w (ESC merge) and e (ESC
-    radix) classes (R1: every class but the atomic ones — CTA hash, long rows — is
-    order-fixed)."""
+    radix) classes (R1: every class is order-fixed)."""
     import paper_1504_05022_b200 as sg
     flags = getattr(sg, flags_name) if flags_name else 0
     A, B = _wide_pair(5, [1, 3, 10, 20, 40, 100] * 6)
@@ -390,3 +391,49 @@ def test_esc_bitexact_vs_oracle_real():
     R = oracle.spgemm(A, B)
     np.testing.assert_array_equal(g["ci"], R.ci)
     np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+@pytest.mark.parametrize("mode", ["int", "real"])
+def test_long_multi_tile(flags_name, mode):
+    """Long rows whose column window spans many bitmap tiles (a 8 Ki-column tile knob against
+    windows of up to 400 000 columns): the tile loop of the count and rank kernels, with every
+    b_j* cut to the tile by binary search.  Structure exact; values bit-identical to the
+    oracle in both value modes (each column is summed by one warp in j order, [P:121-135]),
+    and run to run."""
+    import paper_1504_05022_b200 as sg
+    flags = getattr(sg, flags_name) if flags_name else 0
+    B = gen.random_rows(2000, 400_000, np.full(2000, 64), seed=31, mode=mode)
+    A = gen.random_rows(60, 2000, np.array([1, 3, 10, 20, 40, 100, 300] * 8 + [2, 5, 7, 9]), seed=32, mode=mode)
+    sg.set_debug(-1, 0, 40)          # every row with min(u, n) > 40 takes the long path
+    sg.set_debug_long_tile(8192)     # tiles of 8 Ki (values) / 16 Ki (count) columns
+    g = run_gpu(A, B, flags=flags, stats=True)
+    g2 = run_gpu(A, B, flags=flags)
+    R = oracle.spgemm(A, B)
+    assert g["stats"]["long_rows"] > 0
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+    np.testing.assert_array_equal(g2["val"].view(np.int64), g["val"].view(np.int64))
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+@pytest.mark.parametrize("tier", [13, 14, 15, 20])
+def test_long_and_chash_bitexact_real(flags_name, tier):
+    """The CTA-hash classes (values by the rank kernel) and the long rows accumulate each
+    column in j-ascending order without atomics: real-mode values bit-identical to the oracle
+    and to a second run, including the growth path of the hybrid strategy."""
+    import paper_1504_05022_b200 as sg
+    flags = getattr(sg, flags_name) if flags_name else 0
+    us = [40, 100, 300, 700, 1500, 3000, 6000, 9000]
+    A, B = gen.forced_u_pair(us * 4, n=30000, seed=tier + 90, mode="real", dup=0.6)
+    sg.set_debug(tier, 256 if tier == 20 else 0, 40 if tier == 20 else 0)
+    g = run_gpu(A, B, flags=flags, stats=True)
+    g2 = run_gpu(A, B, flags=flags)
+    R = oracle.spgemm(A, B)
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+    np.testing.assert_array_equal(g2["val"].view(np.int64), g["val"].view(np.int64))
+    from paper_1504_05022_b200 import TIER_NAMES
+    assert TIER_NAMES[tier] in g["stats"]["tier_rows"]
