@@ -142,7 +142,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def run_gpu(args):
+def gpu_context(args):
     import torch
     import torch.distributed as dist
 
@@ -156,27 +156,34 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    flags = sg.FLAG_PRECISE if args.strategy == "precise" else 0
-    work = make_workload(args.config, args.scale)
-    stream = torch.cuda.Stream()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    lib = sg.load()
-
-    # inputs resident in HBM
-    dev_inputs = []
-    prev_is_out = False
-    for name, A, B in work:
-        dA = sg.DeviceCsr.from_host(A)
-        dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
-        dev_inputs.append((name, A, B, dA, dB))
-        prev_is_out = prev_is_out or isinstance(B, str)
-    torch.cuda.synchronize()
-
+    ctx = dict(torch=torch, dist=dist, sg=sg, world=world, rank=rank, local=local,
+               stream=torch.cuda.Stream(), flush=torch.empty(512 << 20, dtype=torch.uint8, device="cuda"))
+    sg.load()
     uid = None
     if world > 1:
         obj = [sg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    ctx["uid"] = uid
+    return ctx
+
+
+def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True):
+    """Time `steps` whole-hot-path steps of workload `cfg` (after `warmup`); returns the
+    bench-line fields (value, ms, hbm, roofline, clocks, ...) plus the inputs for e2e."""
+    torch, dist, sg = ctx["torch"], ctx["dist"], ctx["sg"]
+    world, rank, local = ctx["world"], ctx["rank"], ctx["local"]
+    stream, flush, uid = ctx["stream"], ctx["flush"], ctx["uid"]
+    flags = sg.FLAG_PRECISE if strategy == "precise" else 0
+    work = make_workload(cfg, args.scale if cfg == args.config else None)
+
+    # inputs resident in HBM
+    dev_inputs = []
+    for name, A, B in work:
+        dA = sg.DeviceCsr.from_host(A)
+        dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
+        dev_inputs.append((name, A, B, dA, dB))
+    torch.cuda.synchronize()
 
     dist_ops = {}
 
@@ -185,7 +192,7 @@ def run_gpu(args):
     # all-gathered for the global row offsets.  Other configs: one block (dist_* for N > 1).
     def plan_blocks(A, Bm):
         m = A.shape[0]
-        if args.config != "c5" or Bm is None or isinstance(Bm, str):
+        if cfg != "c5" or Bm is None or isinstance(Bm, str):
             return [(0, m)]
         r0, r1 = (rank * m) // world, ((rank + 1) * m) // world
         bl = np.diff(Bm.rp)
@@ -200,7 +207,7 @@ def run_gpu(args):
     blocks_of = {}
     for (name, A, B, dA, dB) in dev_inputs:
         blocks_of[name] = plan_blocks(A, A if B is None else B)
-    sharded = args.config == "c5"
+    sharded = cfg == "c5"
 
     def one_step(collect=False):
         """Whole hot path once: every product of the workload, symbolic + numeric."""
@@ -250,7 +257,7 @@ def run_gpu(args):
 
     # warm-up (also warms the stream-ordered pool)
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             one_step()
     torch.cuda.synchronize()
     _, info = one_step(collect=True)
@@ -262,7 +269,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         ev = []
         with ClockSampler(local) as cs:
-            for _ in range(args.steps):
+            for _ in range(steps):
                 flush.zero_()  # L2 flush outside the timed window (512 MiB > 126 MB L2)
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
@@ -288,7 +295,7 @@ def run_gpu(args):
             and not clocks["reasons"]):
         ms_total, clocks2 = timed_pass()  # re-measure once
         clocks = dict(clocks2, remeasured=True, first_reasons=clocks["reasons"])
-    ms_step = ms_total / args.steps
+    ms_step = ms_total / steps
 
     # ---------------- per-step accounting (from the collected pass) ----------------
     sum_u = sum(st["sum_u"] if world == 1 else 0 for _, st, _, _, _ in info)
@@ -328,29 +335,28 @@ def run_gpu(args):
 
     # dominant kernel: the largest of (a) the symbolic stage-3 pass of the
     # precise strategy (structure kernels) and (b) each stage-3 class launch that writes values
-    # (numeric classes in precise, the single pass in hybrid); algorithmic bytes per launch:
-    #   rows·(row pointers, perm, offsets, nnz)  +  A entries  +  B read once (≤ products)
-    #   + output entries (C~ or C, 12 B) + the structure set (4 B, write in symbolic / read in
-    #   numeric dense classes)
-    hybrid = args.strategy == "hybrid"
+    # (numeric classes in precise, the single pass in hybrid).  Algorithmic bytes per launch
+    # are SURVEY §8(d)'s per-unit figures (stage 3): 16 B per row, 12 B per A entry, 12 B per
+    # B entry read once (at most one per product), 12 B per output entry; the structure-only
+    # symbolic pass reads 4 B column indices of A and B.  Bytes the implementation adds on top
+    # (its own structure set, perm, C~ offsets) are not counted.
+    hybrid = strategy == "hybrid"
     cands = []
     for name0, st0, nnz0, dA0, Bm0 in info:
         m0 = dA0.rows
         if not hybrid:
             sym_ms = st0["stage_ms"][1]
-            alg = 28 * m0 + 4 * dA0.nnz + 4 * min(Bm0.nnz, st0["sum_u"]) + 4 * nnz0
-            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bwrow STRUCT / k_wrow, k_cta_hash COUNT)" % name0,
-                          "symbolic"))
+            alg = 16 * m0 + 4 * dA0.nnz + 4 * min(Bm0.nnz, st0["sum_u"])
+            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bw_struct2 / k_wrow / k_cta_hash COUNT / "
+                          "k_long_bm_count)" % name0, "symbolic"))
         for cls_name, c in st0["classes"].items():
             if c["ms"] <= 0:
                 continue
-            dense = (not hybrid) and cls_name == "bw"
-            alg = (36 if dense else 28) * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + \
-                12 * c["c_entries"] + (4 * c["c_entries"] if dense else 0)
-            kname = "k_bwrow / k_bw_struct2" if cls_name == "bw" else \
-                "k_esc_sort" if cls_name.startswith("w") else \
-                "k_group" if cls_name.startswith("g") else "k_esc_sort" if cls_name.startswith("e") else \
-                "k_cta_hash" if cls_name.startswith("c") else ("k_long" if hybrid else "k_long_bm_fill")
+            alg = 16 * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + 12 * c["c_entries"]
+            kname = ("k_bwrow DENSE" if not hybrid else "k_bw_struct2 FILL") if cls_name == "bw" else \
+                "k_esc_merge" if cls_name.startswith("w") else \
+                "k_group" if cls_name.startswith("g") else "k_esc_sort / k_esc_merge" if cls_name.startswith("e") else \
+                "k_long_rank" if cls_name.startswith("c") else ("k_long + k_long_rank" if hybrid else "k_long_rank")
             cands.append((c["ms"], alg, "%s: stage-3 class %s (%s)" % (name0, cls_name, kname), cls_name))
     best = max(cands, key=lambda x: x[0])
     launch_ms, alg, kern, cls_name = best
@@ -360,36 +366,31 @@ def run_gpu(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            traffic = tj.get("%s/%s/%s" % (args.config, args.strategy, cls_name))
+            traffic = tj.get("%s/%s/%s" % (cfg, strategy, cls_name))
         except Exception:
             traffic = None
-
-    # ---------------- end-to-end through the public API with host buffers ----------------
-    e2e = None
-    if world == 1 and not args.no_e2e and all(len(b) == 1 for b in blocks_of.values()):
-        e2e = e2e_measure(args, work, flags, stream, sum_u)
 
     result = {
         "metric": METRIC,
         "value": round(gflops, 3),
         "unit": "GFlop/s",
         "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": steps,
+        "warmup": warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded generators, gen/; %s)" % ("coef values" if args.config in ("c1", "c2", "c4a", "c4b")
+        "data": "synthetic (seeded generators, gen/; %s)" % ("coef values" if cfg in ("c1", "c2", "c4a", "c4b")
                                                             else "real values"),
-        "config": {"workload": "%s: %s" % (args.config, CONFIGS[args.config]),
-                   "strategy": args.strategy, "sum_u": sum_u, "nnz_c": nnz_c_tot,
+        "config": {"workload": "%s: %s" % (cfg, CONFIGS[cfg]),
+                   "strategy": strategy, "sum_u": sum_u, "nnz_c": nnz_c_tot,
                    "nnz_a": int(sum(d[3].nnz for d in dev_inputs)),
                    "parallelism": "row blocks x%d (dist_* ABI, NCCL)" % world if world > 1 else "1 GPU",
                    "l2": "flushed before every timed step (512 MiB memset, outside the timed window)",
                    "waves": {n: len(b) for n, b in blocks_of.items() if len(b) > 1} or None,
-                   "scale": args.scale},
+                   "scale": args.scale if cfg == args.config else None},
         "hbm": {"compulsory_bytes": cb, "achieved_gbs": round(step_gbs, 1),
                 "frac_of_peak": round(step_gbs / hbm_peak, 4), "peak_gbs": hbm_peak,
                 "peak_source": peak_src},
@@ -397,20 +398,55 @@ def run_gpu(args):
                      "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
                      "traffic": traffic, "alg_bytes_per_launch": int(alg),
-                     "launch_ms": round(launch_ms, 4), "peak_source": peak_src,
+                     "launch_ms": round(launch_ms, 4), "share_of_step": round(launch_ms / ms_step, 4),
+                     "peak_source": peak_src,
                      "timing": "CUDA events recorded by libspgemm on its stream around the launch"},
         "stage_ms": {n: [round(x, 4) for x in st["stage_ms"]] for n, st, _, _, _ in info},
-        "gpu_launches": launches * args.steps,
+        "gpu_launches": launches * steps,
         "clocks": clocks,
     }
-    if e2e:
-        result["e2e"] = e2e
-    if world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(args, work, budget_s=args.cpu_budget)
-    if rank == 0:
-        print(json.dumps(result), flush=True)
     for op in dist_ops.values():
         op.destroy()
+    can_e2e = world == 1 and all(len(b) == 1 for b in blocks_of.values())
+    return result, dict(work=work, flags=flags, sum_u=sum_u, can_e2e=can_e2e)
+
+
+PER_CONFIG = ["c2", "c3a", "c3b", "c4a", "c4b"]
+
+
+def run_gpu(args):
+    ctx = gpu_context(args)
+    torch, dist, sg = ctx["torch"], ctx["dist"], ctx["sg"]
+    world, rank = ctx["world"], ctx["rank"]
+    result, aux = measure(args, ctx, args.config, args.strategy, args.steps, args.warmup)
+    # ---------------- end-to-end through the public API with host buffers ----------------
+    if aux["can_e2e"] and not args.no_e2e:
+        result["e2e"] = e2e_measure(args, aux["work"], aux["flags"], ctx["stream"], aux["sum_u"])
+    if world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(args, aux["work"], budget_s=args.cpu_budget)
+        result["cpu_single_thread"] = cpu_single_thread(args)
+    del aux
+    # ---------------- the other single-GPU configs of BASELINE.json (same protocol) ----------
+    if world == 1 and not args.no_per_config:
+        per = {}
+        for cfg in PER_CONFIG:
+            for strat in (["precise", "hybrid"] if cfg == "c2" else ["precise"]):
+                if cfg == args.config and strat == args.strategy:
+                    continue
+                torch.cuda.empty_cache()
+                sg.trim_workspace_cache(0)
+                r, _ = measure(args, ctx, cfg, strat, args.per_config_steps, 3)
+                per["%s/%s" % (cfg, strat)] = {
+                    "value": r["value"], "unit": "GFlop/s", "ms_per_step": r["ms_per_step"],
+                    "steps": r["steps"], "sum_u": r["config"]["sum_u"], "nnz_c": r["config"]["nnz_c"],
+                    "hbm_frac_of_peak": r["hbm"]["frac_of_peak"],
+                    "roofline": {k: r["roofline"][k] for k in ("kernel", "achieved", "frac", "traffic",
+                                                                "launch_ms", "share_of_step")},
+                    "stage_ms": r["stage_ms"], "clocks_sm_mhz": r["clocks"]["sm_mhz"],
+                    "clock_reasons": r["clocks"]["reasons"]}
+        result["per_config"] = per
+    if rank == 0:
+        print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -491,15 +527,6 @@ def e2e_measure(args, work, flags, stream, sum_u):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def _row_sample(A, budget_products):
-    """Contiguous row block [0, r) of A with at most budget_products products (A·A)."""
-    import oracle
-    u, _ = oracle.upper_bound(A, A, 0, min(A.shape[0], 1 << 22))
-    cs = np.cumsum(u)
-    r = int(np.searchsorted(cs, budget_products)) + 1
-    return max(1, min(r, A.shape[0])), int(cs[min(r, len(cs)) - 1])
-
-
 def cpu_baseline(args, work, budget_s=15.0):
     """The oracle (oracle/, never tuned for this) on the host cores over a bounded sample:
     a leading block of rows of the first product, sized to ~budget_s seconds."""
@@ -535,6 +562,35 @@ def cpu_baseline(args, work, budget_s=15.0):
             "sample": "rows [0, %d) of %s product %s (%d products, %.2f s per pass, %d passes)" % (
                 r, args.config, name, prods, t, reps),
             "cpu": cpu}
+
+
+def cpu_single_thread(args, budget_s=4.0):
+    """The oracle on ONE host thread for configs 1, 2 and 4a, each on a bounded
+    leading block of rows (~budget_s of work): GFlop/s = 2·products / time."""
+    import oracle
+    out = {}
+    for cfg in ("c1", "c2", "c4a"):
+        name, A, B = make_workload(cfg)[0]
+        Bm = A if B is None or isinstance(B, str) else B
+        u_all, sum_u = oracle.upper_bound(A, Bm)
+        cs = np.cumsum(u_all)
+        r_small = int(min(A.shape[0], max(1, np.searchsorted(cs, 2e6) + 1)))
+        t0 = time.perf_counter()
+        oracle.spgemm(A, Bm, 0, r_small, with_bound=False, threads=1)
+        rate = cs[r_small - 1] / max(time.perf_counter() - t0, 1e-6)
+        r = int(min(A.shape[0], max(r_small, np.searchsorted(cs, rate * budget_s) + 1)))
+        reps = 1
+        if r == A.shape[0]:
+            reps = int(min(200, max(1, budget_s * rate / max(cs[-1], 1))))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.spgemm(A, Bm, 0, r, with_bound=False, threads=1)
+        t = (time.perf_counter() - t0) / reps
+        prods = int(cs[r - 1])
+        out[cfg] = {"value": round(2.0 * prods / t / 1e9, 4), "unit": "GFlop/s", "cores": 1, "kind": "oracle",
+                    "sample": "rows [0, %d) of %s product %s (%d of %d products, %d passes)" % (
+                        r, cfg, name, prods, sum_u, reps)}
+    return out
 
 
 def run_reference(args):
@@ -592,6 +648,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--wave-gb", type=float, default=80.0, help="c5: device memory budget per row wave")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the per_config block (other configs)")
+    ap.add_argument("--per-config-steps", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -178,6 +178,23 @@ __device__ __forceinline__ void sh_red_or(unsigned* p, unsigned v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
+// Bits of the products [q0, qe) (at most kChunk) of one b_j* (columns already restricted to
+// the tile at base): the column loads of the whole work item are issued before the shared-
+// memory ORs, so the gathers overlap instead of one round trip per 32 products.
+__device__ __forceinline__ void set_bits(const int32_t* __restrict__ bci, int64_t q0, int64_t qe, int lane,
+                                         int64_t base, unsigned* bm) {
+  constexpr int K = kChunk / 32;
+  unsigned d[K];
+#pragma unroll
+  for (int u = 0; u < K; ++u) {
+    const int64_t q = q0 + 32 * u + lane;
+    d[u] = q < qe ? (unsigned)(__ldg(bci + q) - base) : 0xffffffffu;
+  }
+#pragma unroll
+  for (int u = 0; u < K; ++u)
+    if (d[u] != 0xffffffffu) sh_red_or(&bm[d[u] >> 5], 1u << (d[u] & 31));
+}
+
 // Words of a tile: the row's window in multiples of NT words, at most tmax.
 template <int NT>
 __device__ __forceinline__ int tile_words(int lo, int hi, int64_t tmax) {
@@ -214,10 +231,7 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax)
           int t;
           int64_t q0, qe;
           work_item<kBmNT>(sb, item, t, q0, qe);
-          for (int64_t q = q0 + lane; q < qe; q += 32) {
-            const unsigned d = (unsigned)(__ldg(a.B.ci + q) - base);  // in [0, tbits): restricted
-            sh_red_or(&bm[d >> 5], 1u << (d & 31));                    // line 8: insert
-          }
+          set_bits(a.B.ci, q0, qe, lane, base, bm);  // line 8: insert
         }
         __syncthreads();
       }
@@ -280,10 +294,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
           int t;
           int64_t q0, qe;
           work_item<NT>(sb, item, t, q0, qe);
-          for (int64_t q = q0 + lane; q < qe; q += 32) {
-            const unsigned d = (unsigned)(__ldg(a.B.ci + q) - base);
-            sh_red_or(&bm[d >> 5], 1u << (d & 31));
-          }
+          set_bits(a.B.ci, q0, qe, lane, base, bm);  // line 8: insert
         }
         __syncthreads();
       }
@@ -346,30 +357,65 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
             const int64_t bs = __ldg(a.B.rp + j);
             sb.bs[threadIdx.x] = bs;
             sb.av[threadIdx.x] = __ldg(a.A.val + e);
-#pragma unroll 1
-            for (int k = 0; k <= NW; ++k)
-              s_split[threadIdx.x][k] = bw.z > 0 ? lower_bound_row(a.B.ci, bs, bw.z, bw.x, bw.y, s_cb[k]) : 0;
+            // the NW+1 lower bounds of the warps' column boundaries in b_j*: NW+1 binary
+            // searches advanced in lockstep, so their loads are in flight together
+            int lo_k[NW + 1], hi_k[NW + 1];
+#pragma unroll
+            for (int k = 0; k <= NW; ++k) {
+              const int c = s_cb[k];
+              lo_k[k] = (bw.z == 0 || c <= bw.x) ? 0 : (c > bw.y ? bw.z : 1);
+              hi_k[k] = (bw.z == 0 || c <= bw.x) ? 0 : (c > bw.y ? bw.z : bw.z - 1);
+            }
+            // invariant: bci[bs + lo - 1] < c <= bci[bs + hi] (first < c <= last inside)
+            bool more = true;
+            while (more) {
+              more = false;
+#pragma unroll
+              for (int k = 0; k <= NW; ++k) {
+                if (lo_k[k] < hi_k[k]) {
+                  const int mid = (lo_k[k] + hi_k[k]) >> 1;
+                  if (__ldg(a.B.ci + bs + mid) < s_cb[k]) lo_k[k] = mid + 1;
+                  else hi_k[k] = mid;
+                  more = more || lo_k[k] < hi_k[k];
+                }
+              }
+            }
+#pragma unroll
+            for (int k = 0; k <= NW; ++k) s_split[threadIdx.x][k] = lo_k[k];
           }
           __syncthreads();
           const int na = (int)min(int64_t(NT), a1 - e0);
           for (int t = 0; t < na; ++t) {
             const int s = s_split[t][w], en = s_split[t][w + 1];
             if (s >= en) continue;
-            const int64_t bs = sb.bs[t];
+            const int32_t* __restrict__ sc = a.B.ci + sb.bs[t];
+            const double* __restrict__ sv = a.B.val + sb.bs[t];
             const double at = sb.av[t];
-            for (int q0 = s; q0 < en; q0 += 32) {
-              const int q = q0 + lane;
-              if (q < en) {
-                const int c = __ldg(a.B.ci + bs + q);
-                const double v = __ldg(a.B.val + bs + q);
-                const unsigned d = (unsigned)(c - base);
-                const unsigned wd = d >> 5;
-                const int rank = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u));
-                double* p = ov + done + rank;
-                *p = __dadd_rn(*p, __dmul_rn(at, v));  // lines 6, 9, 11: c_ik += a_ij b_jk
+            // columns inside one b_j* are distinct: the chunks of a segment touch distinct
+            // outputs, so four of them are gathered, ranked and updated together
+            for (int q0 = s; q0 < en; q0 += 128) {
+              double* p[4];
+              double v[4], old[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int q = q0 + 32 * u + lane;
+                p[u] = nullptr;
+                if (q < en) {
+                  const unsigned d = (unsigned)(__ldg(sc + q) - base);
+                  v[u] = __ldg(sv + q);
+                  const unsigned wd = d >> 5;
+                  const int rank = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u));
+                  p[u] = ov + done + rank;
+                }
               }
-              __syncwarp();  // the next segment may add into a column this one just wrote
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (p[u]) old[u] = *p[u];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (p[u]) *p[u] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
             }
+            __syncwarp();  // the next segment may add into a column this one just wrote
           }
           __syncthreads();
         }

@@ -13,6 +13,7 @@
 //                   set), and the STRUCT / FILL fallback for rows with too many blocks
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -155,6 +156,83 @@ __device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_
   }
 }
 
+// The same walk for 32-bit B offsets with the a_ij chunk staged in shared memory: lane e of a
+// chunk writes one 16-byte record {b_j* start, nnz(b_j*), a_ij} to the warp's stage buffer
+// (32 records, 512 B) and every step reads its record with one broadcast LDS.128 — instead of
+// two or three shuffles per b_j* — and the steps of four b_j* are issued back to back (their
+// gathers in flight together).  Records of lanes past the row's end have nnz 0, so the
+// four-step groups need no bounds check: those steps run with every lane idle (act false).
+template <bool VALS, typename Op>
+__device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci, const double* __restrict__ aval,
+                                                const int64_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                                const double* __restrict__ bval, int64_t a0, int64_t a1,
+                                                int lane, unsigned stage, Op&& op) {
+  for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+    const int64_t e = e0 + lane;
+    int bs = 0, len = 0;
+    double av = 0.0;
+    if (e < a1) {
+      const int j = __ldg(aci + e);
+      const int64_t b0 = __ldg(brp + j);
+      bs = (int)b0;
+      len = (int)(__ldg(brp + j + 1) - b0);
+      if (VALS) av = __ldg(aval + e);
+    }
+    __syncwarp();
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stage + 16u * lane), "r"(bs), "r"(len),
+                 "r"(__double2loint(av)), "r"(__double2hiint(av)) : "memory");
+    __syncwarp();
+    const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
+    if (!__any_sync(kFull, len > 32)) {
+      for (int t0 = 0; t0 < nE; t0 += kGroup) {
+        int c[kGroup];
+        double v[kGroup], at[kGroup];
+        bool act[kGroup];
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          int4 r;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(stage + 16u * (t0 + u)) : "memory");
+          act[u] = lane < r.y;
+          const int q = r.x + lane;
+          c[u] = act[u] ? __ldg(bci + q) : kEmptyKey;
+          if (VALS) {
+            at[u] = __hiloint2double(r.w, r.z);
+            v[u] = act[u] ? __ldg(bval + q) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) op(c[u], VALS ? v[u] : 0.0, VALS ? at[u] : 0.0, act[u]);
+      }
+    } else {
+      for (int t = 0; t < nE; ++t) {
+        int4 r;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(stage + 16u * t) : "memory");
+        const double at = VALS ? __hiloint2double(r.w, r.z) : 0.0;
+        for (int q0 = 0; q0 < r.y; q0 += 32) {
+          const bool act = q0 + lane < r.y;
+          const int q = r.x + q0 + lane;
+          const int c = act ? __ldg(bci + q) : kEmptyKey;
+          const double v = (VALS && act) ? __ldg(bval + q) : 0.0;
+          op(c, v, at, act);
+        }
+      }
+    }
+  }
+}
+
+// walk_row_staged when B's offsets fit 32 bits and the kernel has a stage buffer, else walk_row.
+template <bool VALS, typename IT, typename Op>
+__device__ __forceinline__ void walk_any(const Stage3Args& a, int64_t a0, int64_t a1, int lane, unsigned stage,
+                                         Op&& op) {
+  if constexpr (std::is_same<IT, int>::value) {
+    walk_row_staged<VALS>(a.A.ci, a.A.val, a.B.rp, a.B.ci, a.B.val, a0, a1, lane, stage, op);
+  } else {
+    walk_row<VALS, IT>(a, a0, a1, lane, op);
+  }
+}
+
 // Counting (precise symbolic, rows with W > 2^17): an S-slot table per warp, nnz = the
 // number of claimed slots.  Values of these rows are computed by the ESC (esc.cu).
 template <int LOG2S, int NW, typename IT>
@@ -268,7 +346,7 @@ __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
 //   vals double[nv]
 struct BwLayout {
   int nwd, nsw, nvp, nv, ns;
-  unsigned o_sm, o_pre, o_lst, o_vals, bytes;  // per warp, bytes is a multiple of 16
+  unsigned o_sm, o_pre, o_lst, o_vals, o_stage, bytes;  // per warp, bytes is a multiple of 16
 };
 
 __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vmax, int64_t bmax) {
@@ -287,8 +365,11 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
     L.o_pre = off;                               // (end of the zeroed region)
     L.o_vals = off;
     off += 8u * (L.nv + 1);  // + scratch
-    off += 256u;             // a_ij of the current chunk (walk_row's avs)
+    off = (off + 15u) & ~15u;
+    L.o_stage = off;         // a_ij chunk records of walk_row_staged
+    off += 512u;
   } else {
+    L.o_stage = 0;
     const bool fill = mode == MODE_FILL;
     off = 4u * L.nwd;
     L.o_sm = off;
@@ -469,13 +550,12 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     // Lanes of one b_j* hold distinct columns, so no two lanes of an instruction share a slot;
     // successive b_j* are ordered by the warp's in-order shared-memory accesses.
     const unsigned scratch = vals + 8u * unsigned(L.nv);
-    const unsigned avs = MODE == MODE_DENSE ? scratch + 8u : 0u;
-    walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
+    auto accumulate = [=](int c, double v, double at, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       unsigned word, base;
       if (MODE == MODE_DENSE) {  // one 8-byte record: the word's bits and its first rank
-        const unsigned wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
-        const uint2 rec = sh_ld_v2(bits + 8u * wi);
+        // record (slot-1)*32 + (d>>5)%32: bits - 256 + 256 slot + ((d >> 2) & 0xf8)
+        const uint2 rec = sh_ld_v2(bits - 256u + (sh_ld_u16(dir + 2u * (d >> 10)) << 8) + ((d >> 2) & 0xf8u));
         word = rec.x;
         base = rec.y;
       } else {
@@ -486,7 +566,9 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
       sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
-    }, avs);
+    };
+    if (MODE == MODE_DENSE) walk_any<true, IT>(a, a0, a1, lane, bm + L.o_stage, accumulate);
+    else walk_row<true, IT>(a, a0, a1, lane, accumulate);
     __syncwarp();
     double* ov = a.out_val + o;
     for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
@@ -516,7 +598,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
 // FILL (hybrid) adds pre uint16[ns·32] (rank of each word's first bit) and vals double[nv+1].
 struct Bs2Layout {
   int nsw, ns, nv;
-  unsigned o_bits, o_pre, o_vals, bytes;
+  unsigned o_bits, o_pre, o_vals, o_stage, bytes;
 };
 
 __host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns, bool fill, int64_t vmax) {
@@ -528,7 +610,8 @@ __host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns, bool fill,
   L.o_bits = (2u * L.nsw + 15u) & ~15u;
   L.o_pre = L.o_bits + 128u * ns;
   L.o_vals = L.o_pre + (fill ? 64u * ns : 0u);
-  L.bytes = fill ? ((L.o_vals + 8u * (L.nv + 1) + 15u) & ~15u) : L.o_pre;
+  L.o_stage = fill ? ((L.o_vals + 8u * (L.nv + 1) + 15u) & ~15u) : L.o_pre;  // o_pre is 16-aligned
+  L.bytes = L.o_stage + 512u;  // a_ij chunk records of walk_row_staged
   return L;
 }
 
@@ -538,6 +621,7 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
   const unsigned bits = dir + L.o_bits, pre = dir + L.o_pre, vals = dir + L.o_vals;
+  const unsigned stage = dir + L.o_stage, bitsm = bits - 128u;
   const int ns = L.ns, nsw = L.nsw;
   for (unsigned i = lane; i < L.o_pre / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
   __syncwarp();
@@ -551,7 +635,7 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int nslot = 0;  // warp-uniform
-    walk_row<false, IT>(a, a0, a1, lane, [=, &nslot](int c, double, double, bool act) {
+    walk_any<false, IT>(a, a0, a1, lane, stage, [=, &nslot](int c, double, double, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       const unsigned blk = d >> 10;
       unsigned s = act ? sh_ld_u16(dir + 2u * blk) : 1u;
@@ -567,7 +651,8 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
         __syncwarp();
         if (need) s = sh_ld_u16(dir + 2u * blk);
       }
-      if (act && s != 0u) sh_red_or(bits + 4u * ((s - 1u) * 32u + ((d >> 5) & 31u)), 1u << (d & 31));
+      // word (s-1)*32 + (d>>5)%32 of the slots: bits - 128 + 128 s + ((d >> 3) & 0x7c)
+      if (act && s != 0u) sh_red_or(bitsm + (s << 7) + ((d >> 3) & 0x7cu), 1u << (d & 31));
     });
     __syncwarp();
     if (nslot > ns) {
