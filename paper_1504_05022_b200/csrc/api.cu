@@ -45,11 +45,6 @@ __global__ void k_iota(int32_t* p, int64_t n) {
   if (i < n) p[i] = (int32_t)i;
 }
 
-__global__ void k_long_slots(const LongState* st, int64_t n, int64_t* slots) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) slots[i] = long_table_slots(st[i].cap);
-}
-
 __global__ void k_class_sums(int64_t m, const uint8_t* __restrict__ tier, const int64_t* __restrict__ U,
                              const int64_t* __restrict__ arp, const int64_t* __restrict__ nnz_row,
                              unsigned long long* out) {
@@ -123,17 +118,14 @@ struct spgemm_handle_s {
   // long rows
   int64_t nlong = 0, long_first = 0;
   LongState* lst = nullptr;
-  int32_t** lkeys = nullptr;
-  double** lvals = nullptr;
-  int32_t** lold_keys = nullptr;
-  double** lold_vals = nullptr;
-  int64_t* lold_slots = nullptr;
-  int32_t* lact = nullptr;
-  int32_t* lovf = nullptr;
+  int32_t* lact = nullptr;       // active long rows of a round
+  int32_t* lovf = nullptr;       // rows that checkpointed (overflowed) in a round
   int32_t* lovf_cnt = nullptr;
-  int32_t* liota = nullptr;
-  int64_t* lslots = nullptr;
-  int64_t* lslot_off = nullptr;
+  int64_t* lsizes = nullptr;     // per listed row: entries to add
+  int64_t* loff = nullptr;       // their exclusive scan
+  int64_t* ltable = nullptr;     // chunk tables [nlong][kMaxChunks]
+  int log2c0 = 14;
+  VmmArena arena_col, arena_val;  // long-row arena (hybrid), grown in place
   int64_t long_entries = 0;
   int32_t growth_rounds = 0;
   int64_t tier_count[NUM_TIERS] = {};
@@ -208,8 +200,13 @@ void free_symbolic(spgemm_handle_t h) {
   h->ctil_val = nullptr;
   h->work_ctr = nullptr;
   h->lst = nullptr;
-  h->lkeys = h->lold_keys = nullptr;
-  h->lvals = h->lold_vals = nullptr;
+  h->lact = h->lovf = h->lovf_cnt = nullptr;
+  h->lsizes = h->loff = h->ltable = nullptr;
+  if (h->arena_col.base || h->arena_val.base) {
+    cudaStreamSynchronize(h->stream);  // unmapping is immediate, not stream-ordered
+    vmm_release(&h->arena_col);
+    vmm_release(&h->arena_val);
+  }
   h->nlong = 0;
   h->long_entries = 0;
   h->growth_rounds = 0;
@@ -247,135 +244,94 @@ struct Trace {
   }
 };
 
-// Allocate tables for the long rows listed in `list` (device, nlist entries) whose slot
-// counts are in h->lslots[0..nlist); assign pointers (moving the current ones to old_*).
-spgemm_status_t long_alloc_tables(spgemm_handle_t h, const int32_t* list, int64_t nlist, bool fill,
-                                  bool keep_old) {
-  CK(h, launch_exclusive_scan(h->lslots, h->lslot_off, nlist, h->scan_tmp, h->stream));
-  CK(h, cudaMemcpyAsync(h->pinned, h->lslot_off + nlist, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+// Long-row arena: positions [bump, bump + Σ sizes) for the rows in `list` (NULL: all long
+// rows), mapped on demand in the VMM arenas, and their chunk tables.
+spgemm_status_t long_grow_arena(spgemm_handle_t h, const int32_t* list, int64_t nlist) {
+  CK(h, launch_exclusive_scan(h->lsizes, h->loff, nlist, h->scan_tmp, h->stream));
+  CK(h, cudaMemcpyAsync(h->pinned, h->loff + nlist, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   spgemm_status_t s = sync(h);
   if (s != SPGEMM_SUCCESS) return s;
   const int64_t total = h->pinned[0];
-  int32_t* kb = nullptr;
-  double* vb = nullptr;
-  AL(h, &kb, total);
-  if (fill) AL(h, &vb, total);
-  h->long_entries += total / 2;
-  CK(h, launch_long_assign(list, nlist, h->lslot_off, kb, vb, h->lkeys, h->lvals,
-                           keep_old ? h->lold_keys : nullptr, keep_old ? h->lold_vals : nullptr,
-                           h->lold_slots, h->lst, h->stream));
+  const int64_t end = h->long_entries + total;
+  CK(h, vmm_ensure(&h->arena_col, size_t(end) * sizeof(int32_t)));
+  CK(h, vmm_ensure(&h->arena_val, size_t(end) * sizeof(double)));
+  CK(h, launch_long_assign(h->lst, list, nlist, h->loff, h->long_entries, h->ltable, h->log2c0, h->stream));
+  h->long_entries = end;
   return SPGEMM_SUCCESS;
 }
 
-// Long-row path: progressive allocation with checkpoint / 2x growth / relaunch ([P:297]).
-spgemm_status_t run_long(spgemm_handle_t h, int mode) {
+// Long rows of the hybrid strategy: the paper's group 5 with progressive allocation
+// ([P:297]).  Every long row starts with C0 entries (16 Ki; SPGEMM_FLAG_UPPER_BOUND: min(u_i,
+// n)) in the long-row arena and runs the bitmap rank kernel tile by tile; a tile that does not
+// fit is the checkpoint.  The host then grows each checkpointed row 2x (as many doublings as
+// the tile needs, never above min(u_i, n): reading Q8), maps the new chunks at the arena's
+// end (VMM: nothing written moves, no dump / reload copy) and relaunches only those rows,
+// which resume at their checkpointed tile.
+spgemm_status_t run_long(spgemm_handle_t h) {
   const int64_t nl = h->nlong;
   if (nl == 0) return SPGEMM_SUCCESS;
-  const bool fill = mode == MODE_FILL;
   AL(h, &h->lst, nl);
-  AL(h, &h->lkeys, nl);
-  AL(h, &h->lvals, nl);
-  AL(h, &h->lold_keys, nl);
-  AL(h, &h->lold_vals, nl);
-  AL(h, &h->lold_slots, nl);
   AL(h, &h->lact, nl);
   AL(h, &h->lovf, nl);
-  AL(h, &h->liota, nl);
   AL(h, &h->lovf_cnt, 1);
-  AL(h, &h->lslots, nl);
-  AL(h, &h->lslot_off, nl + 1);
-  CK(h, cudaMemsetAsync(h->lkeys, 0, sizeof(int32_t*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lvals, 0, sizeof(double*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_keys, 0, sizeof(int32_t*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_vals, 0, sizeof(double*) * nl, h->stream));
-  CK(h, cudaMemsetAsync(h->lold_slots, 0, sizeof(int64_t) * nl, h->stream));
-  const unsigned g = (unsigned)((nl + 255) / 256);
-  k_iota<<<g, 256, 0, h->stream>>>(h->liota, nl);
-  const int64_t cap0 = (h->flags & SPGEMM_FLAG_UPPER_BOUND) ? INT64_MAX / 4 : g_long_cap0;
-  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, cap0, h->A, h->B, h->stream));
-  k_long_slots<<<g, 256, 0, h->stream>>>(h->lst, nl, h->lslots);
-  spgemm_status_t s = long_alloc_tables(h, h->liota, nl, fill, false);
+  AL(h, &h->lsizes, nl);
+  AL(h, &h->loff, nl + 1);
+  AL(h, &h->ltable, nl * kMaxChunks);
+  AL(h, &h->work_ctr, 1);
+  int64_t c0 = 1;
+  h->log2c0 = 0;
+  while (c0 < g_long_cap0) {
+    c0 <<= 1;
+    ++h->log2c0;
+  }
+  const int64_t cap0 = (h->flags & SPGEMM_FLAG_UPPER_BOUND) ? INT64_MAX / 4 : c0;
+  // virtual ranges for the arena: the device's memory size (physical pages come on demand)
+  size_t freeb = 0, totalb = 0;
+  CK(h, cudaMemGetInfo(&freeb, &totalb));
+  CK(h, vmm_reserve(&h->arena_col, totalb / 2));
+  CK(h, vmm_reserve(&h->arena_val, totalb));
+  h->long_entries = 0;
+  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, cap0, h->lsizes, h->stream));
+  spgemm_status_t s = long_grow_arena(h, nullptr, nl);
   if (s != SPGEMM_SUCCESS) return s;
-  CK(h, cudaMemcpyAsync(h->lact, h->liota, sizeof(int32_t) * nl, cudaMemcpyDeviceToDevice, h->stream));
+  const unsigned g = (unsigned)((nl + 255) / 256);
+  k_iota<<<g, 256, 0, h->stream>>>(h->lact, nl);
   int64_t nactive = nl;
-  for (int round = 0;; ++round) {
+  for (;;) {
     CK(h, cudaMemsetAsync(h->lovf_cnt, 0, sizeof(int32_t), h->stream));
-    LongArgs la{};
-    la.A = h->A;
-    la.B = h->B;
-    la.n = h->n;
-    la.perm = h->ws.perm;
-    la.first = h->long_first;
-    la.st = h->lst;
-    la.keys = h->lkeys;
-    la.vals = h->lvals;
-    la.old_keys = h->lold_keys;
-    la.old_vals = h->lold_vals;
-    la.old_slots = h->lold_slots;
-    la.active = h->lact;
-    la.nactive = nactive;
-    la.overflow_list = h->lovf;
-    la.overflow_cnt = h->lovf_cnt;
-    la.nnz_row = h->nnz_row;
-    la.mode = mode;
-    CK(h, launch_long(la, h->stream));
+    Stage3Args a{};
+    a.A = h->A;
+    a.B = h->B;
+    a.b_nnz = h->b_nnz;
+    a.n = h->n;
+    a.perm = h->ws.perm;
+    a.first = h->long_first;
+    a.count = nactive;
+    a.nnz_row = h->nnz_row;
+    a.mode = MODE_FILL;
+    a.bwin = h->ws.bwin;
+    a.work_ctr = h->work_ctr;
+    a.lst = h->lst;
+    a.active = h->lact;
+    a.chunk_table = h->ltable;
+    a.arena_col = static_cast<int32_t*>(h->arena_col.base);
+    a.arena_val = static_cast<double*>(h->arena_val.base);
+    a.log2c0 = h->log2c0;
+    a.ovf_list = h->lovf;
+    a.ovf_cnt = h->lovf_cnt;
+    CK(h, launch_long_bitmap(a, h->stream));
     CK(h, cudaMemcpyAsync(h->pinned + 1, h->lovf_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     s = sync(h);
     if (s != SPGEMM_SUCCESS) return s;
     const int64_t novf = *reinterpret_cast<int32_t*>(h->pinned + 1);
     if (novf == 0) break;
-    // host grows the allocation 2x and relaunches the overflowed rows ([P:297])
-    ++h->growth_rounds;
-    CK(h, launch_long_grow(h->lst, h->lovf, novf, h->lslots, h->lold_slots, h->stream));
-    s = long_alloc_tables(h, h->lovf, novf, fill, true);
+    ++h->growth_rounds;  // host grows the checkpointed rows and relaunches them ([P:297])
+    CK(h, launch_long_grow(h->lst, h->lovf, novf, h->lsizes, h->stream));
+    s = long_grow_arena(h, h->lovf, novf);
     if (s != SPGEMM_SUCCESS) return s;
     std::swap(h->lact, h->lovf);
     nactive = novf;
   }
-  return SPGEMM_SUCCESS;
-}
-
-__global__ void k_gather_long_nnz(const int32_t* __restrict__ perm, int64_t first, int64_t nlong,
-                                  const int64_t* __restrict__ nnz_row, int64_t* __restrict__ out) {
-  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < nlong) out[k] = nnz_row[perm[first + k]];
-}
-
-// Hybrid long rows after the progressive structure pass: an arena of exactly nnz(c_i*)
-// entries per long row (columns + values), then the rank kernel writes each row there in
-// order with values accumulated in the oracle's order (longbm.cu).
-spgemm_status_t long_values_hybrid(spgemm_handle_t h) {
-  const int64_t nl = h->nlong;
-  const unsigned g = (unsigned)((nl + 255) / 256);
-  k_gather_long_nnz<<<g, 256, 0, h->stream>>>(h->ws.perm, h->long_first, nl, h->nnz_row, h->lslots);
-  CK(h, cudaGetLastError());
-  CK(h, launch_exclusive_scan(h->lslots, h->lslot_off, nl, h->scan_tmp, h->stream));
-  CK(h, cudaMemcpyAsync(h->pinned, h->lslot_off + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-  spgemm_status_t s = sync(h);
-  if (s != SPGEMM_SUCCESS) return s;
-  const int64_t total = h->pinned[0];
-  int32_t* kb = nullptr;
-  double* vb = nullptr;
-  AL(h, &kb, total);
-  AL(h, &vb, total);
-  h->long_entries = total;
-  CK(h, launch_long_assign(h->liota, nl, h->lslot_off, kb, vb, h->lkeys, h->lvals, nullptr, nullptr,
-                           h->lold_slots, h->lst, h->stream));
-  Stage3Args a{};
-  a.A = h->A;
-  a.B = h->B;
-  a.b_nnz = h->b_nnz;
-  a.n = h->n;
-  a.perm = h->ws.perm;
-  a.first = h->long_first;
-  a.count = nl;
-  a.mode = MODE_FILL;
-  a.bwin = h->ws.bwin;
-  a.row_col = h->lkeys;
-  a.row_val = h->lvals;
-  AL(h, &h->work_ctr, 1);
-  a.work_ctr = h->work_ctr;
-  CK(h, launch_long_bitmap(a, h->stream));
   return SPGEMM_SUCCESS;
 }
 
@@ -611,16 +567,12 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->long_first = h->tier_off[T_LONG];
   if (h->nlong > 0) cudaEventRecord(h->tev[T_LONG][0], h->stream);
   if (hybrid) {
-    // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297] finds
-    // each long row's columns; its values then go, in the oracle's order, into an arena of
-    // exactly nnz(c_i*) entries per row (the row's C~ slice, copied by stage 4)
-    s = run_long(h, MODE_COUNT);
+    // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297]; the
+    // rows' sorted results (values in the oracle's order) are their C~ slices in the long-row
+    // arena, copied by stage 4
+    s = run_long(h);
     if (s != SPGEMM_SUCCESS) return s;
-    if (h->nlong > 0) {
-      s = long_values_hybrid(h);
-      if (s != SPGEMM_SUCCESS) return s;
-      h->launches_sym += 4 + 6 * h->growth_rounds + 6;
-    }
+    if (h->nlong > 0) h->launches_sym += 8 + 7 * h->growth_rounds;
   } else if (h->nlong > 0) {
     // precise: structure of long rows from a bitmap over the column window
     Stage3Args a{};
@@ -699,8 +651,10 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
     ca.tier = h->ws.tier;
     ca.ctil_col = h->ctil_col;
     ca.ctil_val = h->ctil_val;
-    ca.long_keys = h->lkeys;
-    ca.long_vals = h->lvals;
+    ca.chunk_table = h->ltable;
+    ca.arena_col = static_cast<const int32_t*>(h->arena_col.base);
+    ca.arena_val = static_cast<const double*>(h->arena_val.base);
+    ca.log2c0 = h->log2c0;
     ca.c_col = c_col_idx;
     ca.c_val = c_val;
     if (precise) {
@@ -758,10 +712,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
       ca.m = 0;     // nothing to copy: every row was written straight into C
       ca.nlong = 0;
     }
-    const double avg = double(h->nnz_c) / double(h->m);
-    const int group = env_int("SPGEMM_COPY_GROUP", 0);  // 0 = flat warp copy (default)
-    (void)avg;
-    CK(h, launch_copy(ca, group, h->stream));
+    CK(h, launch_copy(ca, h->stream));
     h->launches_num += (ca.m > 0 ? 1 : 0) + (ca.nlong > 0 ? 1 : 0);
   }
   cudaEventRecord(h->ev[5], h->stream);

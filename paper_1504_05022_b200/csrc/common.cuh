@@ -167,6 +167,8 @@ struct CsrView {
 // accumulated into a dense, already ordered array (no insertion, no sort).
 enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1, MODE_STRUCT = 2, MODE_DENSE = 3 };
 
+struct LongState;
+
 struct Stage3Args {
   CsrView A, B;
   int64_t n;
@@ -190,8 +192,17 @@ struct Stage3Args {
   int32_t* bw_ovf_cnt;        //   (re-run over the full-window bitmap; device counter)
   const int32_t* count_dev;   // if set, the kernel reads its row count here (rows = perm[0..))
   int* work_ctr;              // long rows: dynamic row counter (zeroed by the launcher)
-  int32_t* const* row_col;    // bitmap FILL: per work index r, the row's output columns
-  double* const* row_val;     //   and values (hybrid long-row arena); NULL: out_* at out_off
+  // bitmap FILL, progressive mode (hybrid long rows): work index r -> long row active[r];
+  // output through the row's chunk table into the arena; a tile that does not fit the row's
+  // capacity checkpoints the row into ovf_list
+  LongState* lst;
+  const int32_t* active;
+  const int64_t* chunk_table;  // [nlong][kMaxChunks]
+  int32_t* arena_col;
+  double* arena_val;
+  int log2c0;
+  int32_t* ovf_list;
+  int32_t* ovf_cnt;
 };
 // Long-row bitmap tile width in 32-column words (spgemm_set_debug_long_tile; 0 = default).
 extern int64_t g_long_tile_words;
@@ -252,53 +263,52 @@ int64_t scan_tmp_elems(int64_t len);
 cudaError_t launch_exclusive_scan(const int64_t* x, int64_t* y, int64_t len, int64_t* tmp,
                                   cudaStream_t s);
 
-// Long-row (T_LONG) progressive path --------------------------------------------------
-struct LongState {
-  int64_t next_a;   // checkpoint: index of the next unprocessed a_ij ([P:297])
-  int64_t cap;      // current capacity in entries (table has 2*cap slots)
-  int64_t capmax;   // min(u_i, n)
-  int64_t count;    // distinct keys so far
-  int32_t lo, hi;   // column window of the row
-  int32_t done;
-  int32_t pad;
-};
-// Slots of a long-row table of nominal capacity cap: a power of two >= 2·cap.
-__host__ __device__ inline int64_t long_table_slots(int64_t cap) {
-  int64_t s = 2;
-  while (s < 2 * cap) s <<= 1;
-  return s;
+// Long-row (T_LONG) progressive path (hybrid strategy, [P:297]) ------------------------
+// Every long row owns a growable slice of the long-row arena, addressed through a table of
+// chunks: chunk 0 holds positions [0, C0), chunk g >= 1 positions [C0·2^(g-1), C0·2^g) (C0 a
+// power of two), i.e. each 2x growth adds one chunk and nothing already written moves.  The
+// table entry of chunk g is (arena offset of the chunk) - (its first position), so position
+// p of the row lives at arena[table[chunk_of(p)] + p].
+constexpr int kMaxChunks = 34;
+__host__ __device__ inline int chunk_of(int64_t p, int log2c0) {
+  const uint64_t q = uint64_t(p) >> log2c0;
+  if (q == 0) return 0;
+#ifdef __CUDA_ARCH__
+  return 64 - __clzll((long long)q);
+#else
+  return 64 - __builtin_clzll(q);
+#endif
+}
+__host__ __device__ inline int chunks_for(int64_t cap, int log2c0) {  // chunks covering [0, cap)
+  return cap <= 0 ? 0 : chunk_of(cap - 1, log2c0) + 1;
 }
 
-struct LongArgs {
-  CsrView A, B;
-  int64_t n;
-  const int32_t* perm;
-  int64_t first;          // perm index of long row 0
-  LongState* st;          // [nlong]
-  int32_t** keys;         // [nlong] table pointers (current)
-  double** vals;
-  int32_t** old_keys;     // [nlong] previous tables (reload on growth), may hold NULL
-  double** old_vals;
-  int64_t* old_slots;     // [nlong]
-  const int32_t* active;  // list of long-row indices to run
-  int64_t nactive;
-  int32_t* overflow_list; // out: overflowed long-row indices
-  int32_t* overflow_cnt;  // out: count
-  int64_t* nnz_row;       // by row id
-  int mode;
+struct LongState {
+  int64_t next_col;  // checkpoint: first column of the next tile to compute ([P:297]); INT64_MIN = row start
+  int64_t cap;       // current capacity in entries ("we use 2x each time" [P:297])
+  int64_t capmax;    // min(u_i, n): never above the upper bound (reading Q8)
+  int64_t count;     // entries written so far (the tiles before the checkpoint)
+  int64_t need;      // at an overflow: count + the entries of the checkpointed tile; after growth: new cap
 };
-cudaError_t launch_long_init(LongState* st, const int32_t* perm, int64_t first, int64_t nlong,
-                             const int64_t* U, int64_t n, int64_t cap0, CsrView A, CsrView B,
-                             cudaStream_t s);
-cudaError_t launch_long(const LongArgs& a, cudaStream_t s);
-// After an overflow: new cap = min(2*cap, capmax) for rows in `list`; writes slots needed
-// (2*cap) per listed row into slots_out[i].
-cudaError_t launch_long_grow(LongState* st, const int32_t* list, int64_t nlist,
-                             int64_t* slots_out, int64_t* old_slots, cudaStream_t s);
-cudaError_t launch_long_assign(const int32_t* list, int64_t nlist, const int64_t* slot_off,
-                               int32_t* keys_base, double* vals_base, int32_t** keys,
-                               double** vals, int32_t** old_keys, double** old_vals,
-                               int64_t* old_slots, const LongState* st, cudaStream_t s);
+
+cudaError_t launch_long_init(LongState* st, const int32_t* perm, int64_t first, int64_t nlong, const int64_t* U,
+                             int64_t n, int64_t cap0, int64_t* sizes, cudaStream_t s);
+// overflowed rows in `list`: need -> new cap = cap·2^j >= need (capped at capmax); sizes[i] = new - old
+cudaError_t launch_long_grow(LongState* st, const int32_t* list, int64_t nlist, int64_t* sizes, cudaStream_t s);
+// chunk tables of the rows in `list` for positions [old cap, new cap) at arena offsets base + off[i]
+cudaError_t launch_long_assign(LongState* st, const int32_t* list, int64_t nlist, const int64_t* off, int64_t base,
+                               int64_t* table, int log2c0, cudaStream_t s);
+
+// VMM arena (vmm.cu): reserved virtual range, physical memory mapped at its end on demand.
+struct VmmArena {
+  void* base = nullptr;
+  size_t reserved = 0, mapped = 0, gran = 0;
+  int device = 0;
+  void* impl = nullptr;
+};
+cudaError_t vmm_reserve(VmmArena* a, size_t bytes);
+cudaError_t vmm_ensure(VmmArena* a, size_t bytes);
+void vmm_release(VmmArena* a);
 
 // Stage 4 -------------------------------------------------------------------------------
 struct CopyArgs {
@@ -310,12 +320,14 @@ struct CopyArgs {
   const uint8_t* tier;
   const int32_t* ctil_col;
   const double* ctil_val;
-  int32_t* const* long_keys;
-  double* const* long_vals;
+  const int64_t* chunk_table;  // long rows: [nlong][kMaxChunks] into the arena
+  const int32_t* arena_col;
+  const double* arena_val;
+  int log2c0;
   int32_t* c_col;
   double* c_val;
 };
-cudaError_t launch_copy(const CopyArgs& a, int group, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, cudaStream_t s);
 
 // Library-owned stream-ordered pool (one per device, release threshold: keep everything, so
 // warm multiplies allocate without OS calls).  The default device pool is left untouched;

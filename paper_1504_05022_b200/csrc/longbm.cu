@@ -249,8 +249,12 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax)
 
 // --------------------------------------------------------------------- rank fill (values)
 // Output of work index r (position in the class): C's row at out_off[row] (precise, C~
-// classes) or the per-row arena pointers row_col[r] / row_val[r] (hybrid long rows).
-template <int NT>
+// classes); PROG (hybrid long rows, the paper's progressive allocation [P:297]): long row
+// k = active[r], written through its chunk table into the long-row arena; a tile whose
+// entries do not fit the row's current capacity is the checkpoint — the row stops there
+// (earlier tiles stay written), reports how much it needs, and resumes at that tile after the
+// host has grown its allocation.
+template <int NT, bool PROG>
 __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -262,28 +266,39 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
   __shared__ int s_split[NT][NW + 1];
   __shared__ int s_cb[NW + 1];
   __shared__ int64_t s_next;
+  __shared__ int64_t s_tab[PROG ? kMaxChunks : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
-    const int row = __ldg(a.perm + a.first + r);
+    const int k_long = PROG ? __ldg(a.active + r) : 0;
+    const int row = __ldg(a.perm + a.first + (PROG ? int64_t(k_long) : r));
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int32_t* oc;
     double* ov;
-    if (a.row_col) {
-      oc = a.row_col[r];
-      ov = a.row_val[r];
+    int64_t done = 0;  // entries of the row placed by earlier tiles
+    int64_t cap = 0, start = INT64_MIN;
+    if (PROG) {
+      oc = a.arena_col;
+      ov = a.arena_val;
+      const LongState st = a.lst[k_long];
+      done = st.count;
+      cap = st.cap;
+      start = st.next_col;
+      if (threadIdx.x < kMaxChunks) s_tab[threadIdx.x] = a.chunk_table[int64_t(k_long) * kMaxChunks + threadIdx.x];
     } else {
       const int64_t o = __ldg(a.out_off + row);
       oc = a.out_col + o;
       ov = a.out_val + o;
     }
+    // row position p -> element of oc / ov
+    auto at_pos = [&](int64_t p) -> int64_t { return PROG ? s_tab[chunk_of(p, a.log2c0)] + p : p; };
     int lo, hi;
     row_window<NT>(a, a0, a1, s_red, lo, hi);
     const int tw = tile_words<NT>(lo, hi, tmax);
     const int64_t tbits = int64_t(tw) * 32;
     const bool multi = int64_t(hi) - lo + 1 > tbits;
     const int WPT = tw / NT;  // words per thread in the prefix scan
-    int64_t done = 0;         // entries of the row placed by earlier tiles
-    for (int64_t base = lo; base <= hi; base += tbits) {
+    bool overflow = false;
+    for (int64_t base = start == INT64_MIN ? lo : start; base <= hi; base += tbits) {
       const int64_t tend = min(base + tbits, int64_t(hi) + 1);
       for (int k = threadIdx.x; k < tw; k += NT) bm[k] = 0u;
       __syncthreads();
@@ -305,6 +320,18 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
       for (int k = 0; k < WPT; ++k) loc += __popc(bm[threadIdx.x * WPT + k]);
       int T;
       int run = block_excl_scan_i<NT>(loc, &T, s_w);
+      if (PROG && done + T > cap) {
+        // checkpoint ([P:297] "records current computation position"): this tile and the rest
+        // of the row wait for a larger allocation
+        if (threadIdx.x == 0) {
+          a.lst[k_long].next_col = base;
+          a.lst[k_long].count = done;
+          a.lst[k_long].need = done + T;
+          a.ovf_list[atomicAdd(a.ovf_cnt, 1)] = k_long;
+        }
+        overflow = true;
+        break;
+      }
       const int run0 = run;
       for (int k = 0; k < WPT; ++k) {
         const int wi = threadIdx.x * WPT + k;
@@ -313,8 +340,9 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
         int p = run;
         const int cb = (int)(base + int64_t(wi) * 32);
         while (b) {
-          oc[done + p] = cb + __ffs(b) - 1;
-          ov[done + p] = -0.0;
+          const int64_t x = at_pos(done + p);
+          oc[x] = cb + __ffs(b) - 1;
+          ov[x] = -0.0;
           b &= b - 1;
           ++p;
         }
@@ -357,21 +385,39 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
             const int64_t bs = __ldg(a.B.rp + j);
             sb.bs[threadIdx.x] = bs;
             sb.av[threadIdx.x] = __ldg(a.A.val + e);
-            // the NW+1 lower bounds of the warps' column boundaries in b_j*: NW+1 binary
-            // searches advanced in lockstep, so their loads are in flight together
+            // lower bounds of the warps' column boundaries in b_j* (binary searches advanced in
+            // lockstep, their loads in flight together): first the tile's own segment
+            // [s0, s1) (pruned by b_j*'s first / last column), then the NW-1 interior
+            // boundaries inside that segment only
             int lo_k[NW + 1], hi_k[NW + 1];
 #pragma unroll
-            for (int k = 0; k <= NW; ++k) {
+            for (int k = 0; k <= NW; k += NW) {
               const int c = s_cb[k];
               lo_k[k] = (bw.z == 0 || c <= bw.x) ? 0 : (c > bw.y ? bw.z : 1);
               hi_k[k] = (bw.z == 0 || c <= bw.x) ? 0 : (c > bw.y ? bw.z : bw.z - 1);
             }
-            // invariant: bci[bs + lo - 1] < c <= bci[bs + hi] (first < c <= last inside)
-            bool more = true;
-            while (more) {
+            // invariant: bci[bs + lo - 1] < c <= bci[bs + hi]
+            for (bool more = true; more;) {
               more = false;
 #pragma unroll
-              for (int k = 0; k <= NW; ++k) {
+              for (int k = 0; k <= NW; k += NW) {
+                if (lo_k[k] < hi_k[k]) {
+                  const int mid = (lo_k[k] + hi_k[k]) >> 1;
+                  if (__ldg(a.B.ci + bs + mid) < s_cb[k]) lo_k[k] = mid + 1;
+                  else hi_k[k] = mid;
+                  more = more || lo_k[k] < hi_k[k];
+                }
+              }
+            }
+#pragma unroll
+            for (int k = 1; k < NW; ++k) {
+              lo_k[k] = lo_k[0];
+              hi_k[k] = lo_k[NW];
+            }
+            for (bool more = lo_k[0] < lo_k[NW]; more;) {
+              more = false;
+#pragma unroll
+              for (int k = 1; k < NW; ++k) {
                 if (lo_k[k] < hi_k[k]) {
                   const int mid = (lo_k[k] + hi_k[k]) >> 1;
                   if (__ldg(a.B.ci + bs + mid) < s_cb[k]) lo_k[k] = mid + 1;
@@ -405,7 +451,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
                   v[u] = __ldg(sv + q);
                   const unsigned wd = d >> 5;
                   const int rank = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u));
-                  p[u] = ov + done + rank;
+                  p[u] = ov + at_pos(done + rank);
                 }
               }
 #pragma unroll
@@ -423,7 +469,13 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
       done += T;
       __syncthreads();
     }
-    if (threadIdx.x == 0 && a.nnz_row) a.nnz_row[row] = done;
+    if (threadIdx.x == 0 && !overflow) {
+      if (a.nnz_row) a.nnz_row[row] = done;
+      if (PROG) {
+        a.lst[k_long].count = done;
+        a.lst[k_long].next_col = INT64_MAX;
+      }
+    }
     __syncthreads();
   }
 }
@@ -440,6 +492,71 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 }  // namespace
 
 int64_t g_long_tile_words = 0;  // debug knob (spgemm_set_debug_long_tile): 0 = by shared memory
+
+// ------------------------------------------------------------- progressive bookkeeping
+namespace {
+
+__global__ void k_long_init(LongState* st, const int32_t* __restrict__ perm, int64_t first, int64_t nlong,
+                            const int64_t* __restrict__ U, int64_t n, int64_t cap0, int64_t* sizes) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nlong) return;
+  const int64_t u = U[perm[first + k]];
+  LongState s;
+  s.capmax = u < n ? u : n;
+  s.cap = cap0 < s.capmax ? cap0 : s.capmax;
+  s.count = 0;
+  s.next_col = INT64_MIN;
+  s.need = s.cap;
+  st[k] = s;
+  sizes[k] = s.cap;
+}
+
+__global__ void k_long_grow(LongState* st, const int32_t* __restrict__ list, int64_t nlist, int64_t* sizes) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nlist) return;
+  LongState& s = st[list[i]];
+  int64_t c = s.cap;
+  while (c < s.need) c = c * 2 < s.capmax ? c * 2 : s.capmax;  // "we use 2x each time" [P:297]
+  sizes[i] = c - s.cap;
+  s.need = c;  // the new capacity, applied by the assignment
+}
+
+__global__ void k_long_assign(LongState* st, const int32_t* __restrict__ list, int64_t nlist,
+                              const int64_t* __restrict__ off, int64_t base, int64_t* table, int log2c0) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nlist) return;
+  const int k = list ? list[i] : (int)i;
+  LongState& s = st[k];
+  const int64_t old = list ? s.cap : 0;
+  const int64_t cap = s.need;
+  // positions [old, cap) are one contiguous block at base + off[i]: every new chunk maps
+  // position p to (base + off[i]) + (p - old)
+  for (int g = chunks_for(old, log2c0); g < chunks_for(cap, log2c0); ++g)
+    table[int64_t(k) * kMaxChunks + g] = base + off[i] - old;
+  s.cap = cap;
+}
+
+}  // namespace
+
+cudaError_t launch_long_init(LongState* st, const int32_t* perm, int64_t first, int64_t nlong, const int64_t* U,
+                             int64_t n, int64_t cap0, int64_t* sizes, cudaStream_t s) {
+  if (nlong == 0) return cudaSuccess;
+  k_long_init<<<(unsigned)((nlong + 255) / 256), 256, 0, s>>>(st, perm, first, nlong, U, n, cap0, sizes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_long_grow(LongState* st, const int32_t* list, int64_t nlist, int64_t* sizes, cudaStream_t s) {
+  if (nlist == 0) return cudaSuccess;
+  k_long_grow<<<(unsigned)((nlist + 255) / 256), 256, 0, s>>>(st, list, nlist, sizes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_long_assign(LongState* st, const int32_t* list, int64_t nlist, const int64_t* off, int64_t base,
+                               int64_t* table, int log2c0, cudaStream_t s) {
+  if (nlist == 0) return cudaSuccess;
+  k_long_assign<<<(unsigned)((nlist + 255) / 256), 256, 0, s>>>(st, list, nlist, off, base, table, log2c0);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
@@ -461,7 +578,7 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   int per_sm = 1;
   cudaError_t e;
   if (fill) {
-    auto kern = k_long_rank<kRkNT>;
+    auto kern = a.lst ? k_long_rank<kRkNT, true> : k_long_rank<kRkNT, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, sm);
