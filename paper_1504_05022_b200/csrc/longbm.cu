@@ -255,11 +255,12 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax)
 // (earlier tiles stay written), reports how much it needs, and resumes at that tile after the
 // host has grown its allocation.
 template <int NT, bool PROG>
-__global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
+__global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
   int* pre = reinterpret_cast<int*>(smem + size_t(tmax) * sizeof(unsigned));
+  double* vals = reinterpret_cast<double*>(smem + size_t(tmax) * 8);  // V values of a rank window
   __shared__ int s_red[2 * NW];
   __shared__ int s_w[NW + 1];
   __shared__ Batch<NT> sb;
@@ -340,43 +341,39 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
         int p = run;
         const int cb = (int)(base + int64_t(wi) * 32);
         while (b) {
-          const int64_t x = at_pos(done + p);
-          oc[x] = cb + __ffs(b) - 1;
-          ov[x] = -0.0;
+          oc[at_pos(done + p)] = cb + __ffs(b) - 1;
           b &= b - 1;
           ++p;
         }
         run = p;
       }
-      // rank ranges of the warps: warp k owns ranks [floor(k*T/NW), floor((k+1)*T/NW)),
-      // i.e. columns [cb[k], cb[k+1])
-      if (threadIdx.x == 0) {
-        s_cb[0] = (int)base;
-        s_cb[NW] = (int)tend;
-      }
-      for (int k = 1; k < NW; ++k) {
-        const int rk = (int)((int64_t(k) * T) / NW);
-        if (rk >= run0 && rk < run) {  // the word holding rank rk is one of mine
-          int q = run0;
-          for (int kk = 0; kk < WPT; ++kk) {
-            const int wi = threadIdx.x * WPT + kk;
-            unsigned b = bm[wi];
-            const int pc = __popc(b);
-            if (rk < q + pc) {
-              for (int s = rk - q; s > 0; --s) b &= b - 1;  // drop the lower set bits
-              s_cb[k] = (int)(base + int64_t(wi) * 32 + __ffs(b) - 1);
-              break;
+      // 3. values, in windows of at most V consecutive ranks whose values live in shared
+      //    memory.  Inside a window warp k owns the ranks [w0 + floor(k*wn/NW), w0 +
+      //    floor((k+1)*wn/NW)), i.e. the columns [cb[k], cb[k+1]); every warp walks the a_ij
+      //    in j-ascending order and adds, of each b_j*, only the products of its own columns.
+      for (int w0 = 0; w0 < T; w0 += V) {
+        const int wn = min(V, T - w0);
+        for (int k = 0; k <= NW; ++k) {
+          const int rk = w0 + (k < NW ? (int)((int64_t(k) * wn) / NW) : wn);
+          if (rk >= T) {
+            if (threadIdx.x == 0) s_cb[k] = (int)tend;
+          } else if (rk >= run0 && rk < run) {  // the word holding rank rk is one of mine
+            int q = run0;
+            for (int kk = 0; kk < WPT; ++kk) {
+              const int wi = threadIdx.x * WPT + kk;
+              unsigned b = bm[wi];
+              const int pc = __popc(b);
+              if (rk < q + pc) {
+                for (int z = rk - q; z > 0; --z) b &= b - 1;  // drop the lower set bits
+                s_cb[k] = (int)(base + int64_t(wi) * 32 + __ffs(b) - 1);
+                break;
+              }
+              q += pc;
             }
-            q += pc;
           }
         }
-        if (rk >= T) {
-          if (threadIdx.x == 0) s_cb[k] = (int)tend;
-        }
-      }
-      __syncthreads();
-      // 3. values: warp w walks the a_ij in order, its own column range of each b_j*
-      if (T > 0) {
+        for (int i = threadIdx.x; i < wn; i += NT) vals[i] = -0.0;  // the identity of + (line 9)
+        __syncthreads();
         for (int64_t e0 = a0; e0 < a1; e0 += NT) {
           const int64_t e = e0 + threadIdx.x;
           if (e < a1) {
@@ -385,8 +382,8 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
             const int64_t bs = __ldg(a.B.rp + j);
             sb.bs[threadIdx.x] = bs;
             sb.av[threadIdx.x] = __ldg(a.A.val + e);
-            // lower bounds of the warps' column boundaries in b_j* (binary searches advanced in
-            // lockstep, their loads in flight together): first the tile's own segment
+            // lower bounds of the warps' column boundaries in b_j* (binary searches advanced
+            // in lockstep, their loads in flight together): first the window's own segment
             // [s0, s1) (pruned by b_j*'s first / last column), then the NW-1 interior
             // boundaries inside that segment only
             int lo_k[NW + 1], hi_k[NW + 1];
@@ -432,39 +429,40 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
           __syncthreads();
           const int na = (int)min(int64_t(NT), a1 - e0);
           for (int t = 0; t < na; ++t) {
-            const int s = s_split[t][w], en = s_split[t][w + 1];
-            if (s >= en) continue;
+            const int s0 = s_split[t][w], en = s_split[t][w + 1];
+            if (s0 >= en) continue;
             const int32_t* __restrict__ sc = a.B.ci + sb.bs[t];
             const double* __restrict__ sv = a.B.val + sb.bs[t];
             const double at = sb.av[t];
             // columns inside one b_j* are distinct: the chunks of a segment touch distinct
             // outputs, so four of them are gathered, ranked and updated together
-            for (int q0 = s; q0 < en; q0 += 128) {
-              double* p[4];
+            for (int q0 = s0; q0 < en; q0 += 128) {
+              int x[4];
               double v[4], old[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int q = q0 + 32 * u + lane;
-                p[u] = nullptr;
+                x[u] = -1;
                 if (q < en) {
                   const unsigned d = (unsigned)(__ldg(sc + q) - base);
                   v[u] = __ldg(sv + q);
                   const unsigned wd = d >> 5;
-                  const int rank = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u));
-                  p[u] = ov + at_pos(done + rank);
+                  x[u] = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u)) - w0;
                 }
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u)
-                if (p[u]) old[u] = *p[u];
+                if (x[u] >= 0) old[u] = vals[x[u]];
 #pragma unroll
               for (int u = 0; u < 4; ++u)
-                if (p[u]) *p[u] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
+                if (x[u] >= 0) vals[x[u]] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
             }
             __syncwarp();  // the next segment may add into a column this one just wrote
           }
           __syncthreads();
         }
+        for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + w0 + i)] = vals[i];
+        __syncthreads();
       }
       done += T;
       __syncthreads();
@@ -579,13 +577,25 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   cudaError_t e;
   if (fill) {
     auto kern = a.lst ? k_long_rank<kRkNT, true> : k_long_rank<kRkNT, false>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // two CTAs per SM: the rest of a CTA's share of shared memory holds the values of a rank
+    // window (c3b: 64 KB of bits and ranks, 4 Ki values)
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, sm);
+    int dev = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int64_t per_cta = int64_t(smem_sm) / 2 - 1024 - int64_t(fa.sharedSizeBytes);
+    int64_t V = (per_cta - int64_t(sm)) / 8 / 256 * 256;
+    if (V < 1024) V = 1024;
+    const size_t smv = sm + size_t(V) * 8;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smv);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = int64_t(sm_count()) * per_sm;
     if (grid > a.count) grid = a.count;
-    kern<<<(unsigned)grid, nt, sm, s>>>(a, (int)tmax);
+    kern<<<(unsigned)grid, nt, smv, s>>>(a, (int)tmax, (int)V);
   } else {
     e = cudaFuncSetAttribute(k_long_bm_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -718,6 +718,203 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
 }
 
+// ----------------------------------------------------------------------------------------
+// T_BW STRUCT (precise symbolic), 32-bit B offsets: the block-directory bitmap of
+// k_bw_struct2 with the per-step work cut down.
+//  * walk: the a_ij chunk is staged as 16-byte records (one LDS.64 per b_j*); the four steps
+//    of a group load their columns and directory slots first and take ONE vote for first
+//    touches of a block (rare) instead of one per step; slot 0 is a dummy, so idle lanes and
+//    rows past the slot limit OR into it without a branch.
+//  * emission: the row's nonzero words are first compacted, in column order, into a list of
+//    (first column, bits) pairs in the warp's stage buffer; each full list of 32 words costs
+//    one scan, so the per-block scans of k_bw_struct2 (36 % of its instructions on c2) go.
+// Per warp: dir uint16[nsw] | bits uint32[(ns+1)·32] | stage 64 x 8 B.
+struct SymLayout {
+  int nsw, ns;
+  unsigned o_bits, o_stage, bytes;
+};
+
+__host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
+  SymLayout L;
+  const int nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
+  L.nsw = (nwd / 32 + 31) / 32 * 32;
+  L.ns = ns;
+  L.o_bits = (2u * L.nsw + 15u) & ~15u;
+  L.o_stage = L.o_bits + 128u * (ns + 1);
+  L.bytes = L.o_stage + 512u;
+  return L;
+}
+
+__global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
+  extern __shared__ __align__(16) uint32_t s_bw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
+  const unsigned bits = dir + L.o_bits, stage = dir + L.o_stage;
+  const int ns = L.ns, nsw = L.nsw;
+  const int32_t* __restrict__ aci = a.A.ci;
+  const int64_t* __restrict__ brp = a.B.rp;
+  const int32_t* __restrict__ bci = a.B.ci;
+  for (unsigned i = lane; i < L.o_stage / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
+  __syncwarp();
+  const unsigned lt = lanemask_lt_();
+  int bmax = 0;
+
+  const int64_t per = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA (L1 reuse)
+  const int64_t rend = min(int64_t(blockIdx.x) * per + per, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * per + w; r < rend; r += nw) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int nslot = 0;  // warp-uniform
+    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+      const int64_t e = e0 + lane;
+      int bs = 0, len = 0;
+      if (e < a1) {
+        const int j = __ldg(aci + e);
+        const int64_t b0 = __ldg(brp + j);
+        bs = (int)b0;
+        len = (int)(__ldg(brp + j + 1) - b0);
+      }
+      __syncwarp();
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(stage + 8u * lane), "r"(bs), "r"(len) : "memory");
+      __syncwarp();
+      const int nE = (int)min(int64_t(32), a1 - e0);
+      for (int t0 = 0; t0 < nE; t0 += kGroup) {
+        unsigned d[kGroup], sl[kGroup];
+        bool need[kGroup];
+        int nlong = 0;
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));  // lanes past the row: len 0
+          nlong |= (int)rec.y > 32;
+          const bool act = lane < (int)rec.y;
+          d[u] = act ? (unsigned)(__ldg(bci + (int)rec.x + lane) - lo) : 0u;
+          sl[u] = act ? sh_ld_u16(dir + 2u * (d[u] >> 10)) : 0u;  // 0: dummy slot / no slot yet
+          need[u] = act && sl[u] == 0u;
+        }
+        if (__any_sync(kFull, nlong)) {
+          // a b_j* longer than 32 in this group: take the general path for the whole group
+          for (int u = 0; u < kGroup && t0 + u < nE; ++u) {
+            const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));
+            for (int q0 = 0; q0 < (int)rec.y; q0 += 32) {
+              const bool act = q0 + lane < (int)rec.y;
+              const unsigned dd = act ? (unsigned)(__ldg(bci + (int)rec.x + q0 + lane) - lo) : 0u;
+              unsigned s1 = act ? sh_ld_u16(dir + 2u * (dd >> 10)) : 0u;
+              const bool nd = act && s1 == 0u;
+              const unsigned nm = __ballot_sync(kFull, nd);
+              if (nm) {
+                const unsigned blk = dd >> 10;
+                const unsigned bp = __shfl_up_sync(kFull, blk, 1);
+                const bool lead = nd && (lane == 0 || !((nm >> (lane - 1)) & 1u) || bp != blk);
+                const unsigned lm = __ballot_sync(kFull, lead);
+                const int id = nslot + __popc(lm & lt) + 1;
+                if (lead && id <= ns) sh_st_u16(dir + 2u * blk, (unsigned)id);
+                nslot += __popc(lm);
+                __syncwarp();
+                if (nd) s1 = sh_ld_u16(dir + 2u * blk);
+              }
+              sh_red_or(bits + (s1 << 7) + ((dd >> 3) & 0x7cu), act ? 1u << (dd & 31) : 0u);
+            }
+          }
+          continue;
+        }
+        const bool any_need = need[0] || need[1] || need[2] || need[3];
+        if (__any_sync(kFull, any_need)) {
+          // first touch of some blocks: the first lane of each block's run claims a slot,
+          // step by step (the steps' order is the walk's order)
+#pragma unroll
+          for (int u = 0; u < kGroup; ++u) {
+            const unsigned nm = __ballot_sync(kFull, need[u]);
+            if (nm) {
+              const unsigned blk = d[u] >> 10;
+              const unsigned bp = __shfl_up_sync(kFull, blk, 1);
+              const bool lead = need[u] && (lane == 0 || !((nm >> (lane - 1)) & 1u) || bp != blk);
+              const unsigned lm = __ballot_sync(kFull, lead);
+              const int id = nslot + __popc(lm & lt) + 1;
+              if (lead && id <= ns) sh_st_u16(dir + 2u * blk, (unsigned)id);
+              nslot += __popc(lm);
+              __syncwarp();
+#pragma unroll
+              for (int v2 = u; v2 < kGroup; ++v2)  // later steps may touch the same new blocks
+                if (need[v2]) {
+                  sl[v2] = sh_ld_u16(dir + 2u * (d[v2] >> 10));
+                  need[v2] = sl[v2] == 0u;
+                }
+            }
+          }
+        }
+        // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: dummy slot)
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u)
+          sh_red_or(bits + (sl[u] << 7) + ((d[u] >> 3) & 0x7cu), sl[u] ? 1u << (d[u] & 31) : 0u);
+      }
+    }
+    __syncwarp();
+    if (nslot > ns) {
+      // too many blocks: clear and hand the row to the full-window kernel
+      for (int s = 1; s <= ns; ++s) sh_st(bits + 128u * s + 4u * lane, 0u);
+      for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
+      if (lane == 0) a.bw_ovf_list[atomicAdd(a.bw_ovf_cnt, 1)] = row;
+      __syncwarp();
+      continue;
+    }
+    // the sorted column set: nonzero words in column order -> list (stage) -> bits
+    int32_t* oc = a.out_col + __ldg(a.out_off + row);
+    int nnz = 0, nl = 0;
+    auto flush = [&](int cnt) {  // emit list entries [0, cnt) (cnt <= 32)
+      uint2 ent = make_uint2(0u, 0u);
+      if (lane < cnt) ent = sh_ld_v2(stage + 8u * lane);
+      const int pc = __popc(ent.y);
+      const int inc = warp_incl_scan(pc, lane);
+      int32_t* q = oc + nnz + inc - pc;
+      unsigned wd = ent.y;
+      const int cb = (int)ent.x - 1;
+      while (wd) {
+        *q++ = cb + __ffs(wd);
+        wd &= wd - 1;
+      }
+      nnz += __shfl_sync(kFull, inc, 31);
+    };
+    for (int s0 = 0; s0 < nsw; s0 += 32) {
+      const unsigned dl = sh_ld_u16(dir + 2u * (s0 + lane));
+      unsigned nzb = __ballot_sync(kFull, dl != 0u);
+      if (dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
+      while (nzb) {
+        const int b = __ffs(nzb) - 1;
+        nzb &= nzb - 1;
+        const unsigned wa = bits + (__shfl_sync(kFull, dl, b) << 7) + 4u * lane;
+        const unsigned word = sh_ld(wa);
+        const unsigned nzw = __ballot_sync(kFull, word != 0u);
+        if (word) {
+          sh_st(wa, 0u);
+          const int pos = nl + __popc(nzw & lt);  // < 64
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(stage + 8u * pos),
+                       "r"((unsigned)(lo + ((s0 + b) * 32 + lane) * 32)), "r"(word) : "memory");
+        }
+        nl += __popc(nzw);
+        __syncwarp();
+        if (nl >= 32) {
+          flush(32);
+          nl -= 32;
+          __syncwarp();
+          if (lane < nl) {
+            const uint2 rest = sh_ld_v2(stage + 8u * (32 + lane));
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(stage + 8u * lane), "r"(rest.x), "r"(rest.y)
+                         : "memory");
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (nl > 0) flush(nl);
+    bmax = max(bmax, nslot);
+    if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncwarp();
+  }
+  if (lane == 0 && bmax > 0 && a.bw_bmax_out)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
+}
+
 }  // namespace
 
 template <typename K>
@@ -814,6 +1011,22 @@ static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static cudaError_t launch_sym(const Stage3Args& a, cudaStream_t s) {
+  const SymLayout L = sym_layout(a.bw_wmax, kBs2Slots);
+  constexpr int nw = 8;
+  const size_t bytes = size_t(nw) * L.bytes;
+  cudaError_t e = cudaFuncSetAttribute(k_bw_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bw_sym, nw * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.count + nw - 1) / nw;
+  const int64_t cap = int64_t(num_sms()) * per_sm;
+  k_bw_sym<<<(unsigned)(need < cap ? need : cap), nw * 32, bytes, s>>>(a, L);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const int64_t blocks = (a.bw_wmax + 1023) / 1024;
@@ -825,8 +1038,9 @@ cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const bool i32 = a.b_nnz < (int64_t(1) << 31);
     const bool fill = a.mode == MODE_FILL;
+    static const bool old_sym = getenv("SPGEMM_OLD_SYM") != nullptr;  // A/B switch (development)
     e = fill ? (i32 ? launch_bs2<int, true>(a, s) : launch_bs2<int64_t, true>(a, s))
-             : (i32 ? launch_bs2<int, false>(a, s) : launch_bs2<int64_t, false>(a, s));
+             : (i32 ? (old_sym ? launch_bs2<int, false>(a, s) : launch_sym(a, s)) : launch_bs2<int64_t, false>(a, s));
     if (e != cudaSuccess) return e;
     Stage3Args b = a;
     b.perm = a.bw_ovf_list;
