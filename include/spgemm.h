@@ -175,8 +175,29 @@ spgemm_status_t spgemm_dist_create(spgemm_handle_t* handle, int rank, int nranks
                                    const int32_t* b_col_idx, const double* b_val, int64_t b_nnz,
                                    spgemm_stream_t stream, uint32_t flags);
 
-/* Partition + local stages 1-3 + allgather.  Rank owns rows [*row_begin, *row_end) of C
- * (HOST outs); *local_nnz / *global_nnz are HOST outs. */
+/* Sharded inputs (config 5: each rank generates its own share).  Rank r passes the rows
+ * [a_row_begin, a_row_end) of A (the caller's partition, not re-balanced; blocks must cover
+ * A's rows in rank order for the global CSR to be the concatenation) and the rows
+ * [b_row_begin, b_row_end) of B; the B slices of all ranks must tile [0, k) in rank order.
+ * Row pointer arrays have (rows + 1) entries and may start at any value: entry e of a block
+ * is col_idx[e - row_ptr[0]] / val[e - row_ptr[0]].  B is replicated by an all-gather of the
+ * slices (grouped ncclBroadcast, slices placed at their global entry offset, row pointers
+ * rebased); B's values travel on a second stream during the structure-only symbolic pass of
+ * SPGEMM_FLAG_PRECISE.  All pointers are DEVICE pointers and stay owned by the caller (valid
+ * until dist_numeric's work completed).  Errors: INVALID_VALUE (ranges, NULL pointers,
+ * INPUTS_REPLICATED), INDEX_OVERFLOW, NCCL, CUDA. */
+spgemm_status_t spgemm_dist_create_sharded(spgemm_handle_t* handle, int rank, int nranks,
+                                           const uint8_t id[128], int64_t m, int64_t k, int64_t n,
+                                           int64_t a_row_begin, int64_t a_row_end,
+                                           const int64_t* a_row_ptr, const int32_t* a_col_idx,
+                                           const double* a_val, int64_t a_nnz, int64_t b_row_begin,
+                                           int64_t b_row_end, const int64_t* b_row_ptr,
+                                           const int32_t* b_col_idx, const double* b_val,
+                                           int64_t b_nnz, spgemm_stream_t stream, uint32_t flags);
+
+/* Partition + input movement + local stages 1-3 + allgather.  Rank owns rows
+ * [*row_begin, *row_end) of C (HOST outs); *local_nnz / *global_nnz are HOST outs.
+ * Synchronises the handle's stream. */
 spgemm_status_t spgemm_dist_symbolic(spgemm_handle_t handle, int64_t* row_begin,
                                      int64_t* row_end, int64_t* local_nnz, int64_t* global_nnz);
 
@@ -185,11 +206,37 @@ spgemm_status_t spgemm_dist_symbolic(spgemm_handle_t handle, int64_t* row_begin,
 spgemm_status_t spgemm_dist_numeric(spgemm_handle_t handle, int64_t* c_row_ptr,
                                     int32_t* c_col_idx, double* c_val);
 
-/* Host-side partition rule used by dist_symbolic (exposed for tests): given the inclusive
- * prefix sums of u over m rows (HOST array), write nranks+1 split points (HOST):
- * s_0 = 0, s_P = m, s_r = min{ i : scan[i] >= ceil(r·total/P) } clamped monotone. */
+/* ---- host arithmetic of the dist protocol (all HOST pointers; used by dist_symbolic and
+ * exported so that CPU tests drive the same code) ---- */
+
+/* Partition rule: given the inclusive prefix sums of u over m rows, write nranks+1 split
+ * points: s_0 = 0, s_P = m, s_r = min{ i : scan[i] >= ceil(r·total/P) } + 1 clamped
+ * monotone (rank r owns rows [s_r, s_r+1): about Σu/P products each, [P:25]). */
 spgemm_status_t spgemm_partition_rows(const int64_t* u_inclusive_scan, int64_t m, int nranks,
                                       int64_t* splits);
+
+/* Entry ranges of the row blocks: rp_at_splits[r] = A.row_ptr[s_r] (nranks+1 values) ->
+ * entry_bounds[2r], entry_bounds[2r+1] = first / one-past-last entry of rank r's block (the
+ * col_idx / val ranges the root sends).  Errors: INVALID_VALUE, INVALID_CSR (decreasing). */
+spgemm_status_t spgemm_dist_block_entries(const int64_t* rp_at_splits, int nranks,
+                                          int64_t* entry_bounds);
+
+/* Placement of sharded B slices: slice r = rows [row_begin[r], row_end[r]) with nnz[r]
+ * entries; checks that the slices tile [0, k) in rank order and writes entry_base[r] (global
+ * entry offset of slice r) and entry_base[nranks] = nnz(B).  Errors: INVALID_VALUE. */
+spgemm_status_t spgemm_dist_slice_layout(const int64_t* row_begin, const int64_t* row_end,
+                                         const int64_t* nnz, int nranks, int64_t k,
+                                         int64_t* entry_base);
+
+/* Stitching (stage 4's sum across ranks, [P:301]): from every rank's nnz, this rank's
+ * global row-pointer offset and nnz(C). */
+spgemm_status_t spgemm_dist_offsets(const int64_t* local_nnz, int nranks, int rank,
+                                    int64_t* offset, int64_t* total);
+
+/* Test hook: the DEVICE partition kernel of dist_symbolic on a DEVICE inclusive scan (m
+ * entries) -> HOST splits (nranks+1), to hold it against spgemm_partition_rows. */
+spgemm_status_t spgemm_debug_partition(const int64_t* u_inclusive_scan, int64_t m, int nranks,
+                                       int64_t* splits);
 
 #ifdef __cplusplus
 }

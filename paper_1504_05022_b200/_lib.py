@@ -115,8 +115,20 @@ def load():
                                          ctypes.POINTER(I64)]
     lib.spgemm_dist_numeric.restype = st
     lib.spgemm_dist_numeric.argtypes = [H, P, P, P]
+    lib.spgemm_dist_create_sharded.restype = st
+    lib.spgemm_dist_create_sharded.argtypes = [ctypes.POINTER(H), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                               I64, I64, I64, I64, I64, P, P, P, I64, I64, I64, P, P, P, I64, P,
+                                               ctypes.c_uint32]
     lib.spgemm_partition_rows.restype = st
     lib.spgemm_partition_rows.argtypes = [P, I64, ctypes.c_int, P]
+    lib.spgemm_dist_block_entries.restype = st
+    lib.spgemm_dist_block_entries.argtypes = [P, ctypes.c_int, P]
+    lib.spgemm_dist_slice_layout.restype = st
+    lib.spgemm_dist_slice_layout.argtypes = [P, P, P, ctypes.c_int, I64, P]
+    lib.spgemm_dist_offsets.restype = st
+    lib.spgemm_dist_offsets.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    lib.spgemm_debug_partition.restype = st
+    lib.spgemm_debug_partition.argtypes = [P, I64, ctypes.c_int, P]
     _lib = lib
     return lib
 

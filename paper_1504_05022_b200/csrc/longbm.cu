@@ -347,12 +347,14 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
         }
         run = p;
       }
-      // 3. values, in windows of at most V consecutive ranks whose values live in shared
-      //    memory.  Inside a window warp k owns the ranks [w0 + floor(k*wn/NW), w0 +
-      //    floor((k+1)*wn/NW)), i.e. the columns [cb[k], cb[k+1]); every warp walks the a_ij
-      //    in j-ascending order and adds, of each b_j*, only the products of its own columns.
-      for (int w0 = 0; w0 < T; w0 += V) {
-        const int wn = min(V, T - w0);
+      // 3. values.  The tile's ranks are split into NW equal ranges: warp k owns the ranks
+      //    [floor(k*T/NW), floor((k+1)*T/NW)), i.e. the columns [cb[k], cb[k+1]); every warp
+      //    walks the a_ij in j-ascending order and adds, of each b_j*, only the products of its
+      //    own columns.  The values accumulate in shared memory when the tile's T entries fit
+      //    (V of them), else in place in the output (L2).
+      const bool insm = T <= V;
+      {
+        const int w0 = 0, wn = T;
         for (int k = 0; k <= NW; ++k) {
           const int rk = w0 + (k < NW ? (int)((int64_t(k) * wn) / NW) : wn);
           if (rk >= T) {
@@ -372,7 +374,10 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
             }
           }
         }
-        for (int i = threadIdx.x; i < wn; i += NT) vals[i] = -0.0;  // the identity of + (line 9)
+        for (int i = threadIdx.x; i < wn; i += NT) {  // the identity of + (line 9's assignment)
+          if (insm) vals[i] = -0.0;
+          else ov[at_pos(done + i)] = -0.0;
+        }
         __syncthreads();
         for (int64_t e0 = a0; e0 < a1; e0 += NT) {
           const int64_t e = e0 + threadIdx.x;
@@ -450,18 +455,32 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
                   x[u] = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u)) - w0;
                 }
               }
+              if (insm) {
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (x[u] >= 0) old[u] = vals[x[u]];
+                for (int u = 0; u < 4; ++u)
+                  if (x[u] >= 0) old[u] = vals[x[u]];
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (x[u] >= 0) vals[x[u]] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
+                for (int u = 0; u < 4; ++u)
+                  if (x[u] >= 0) vals[x[u]] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
+              } else {
+                double* p[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (x[u] >= 0) {
+                    p[u] = ov + at_pos(done + x[u]);
+                    old[u] = *p[u];
+                  }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (x[u] >= 0) *p[u] = __dadd_rn(old[u], __dmul_rn(at, v[u]));
+              }
             }
             __syncwarp();  // the next segment may add into a column this one just wrote
           }
           __syncthreads();
         }
-        for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + w0 + i)] = vals[i];
+        if (insm)
+          for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + w0 + i)] = vals[i];
         __syncthreads();
       }
       done += T;
@@ -585,7 +604,8 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
     int dev = 0, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    const int64_t per_cta = int64_t(smem_sm) / 2 - 1024 - int64_t(fa.sharedSizeBytes);
+    static const int ctas = getenv("SPGEMM_RANK_CTAS") ? atoi(getenv("SPGEMM_RANK_CTAS")) : 2;
+    const int64_t per_cta = int64_t(smem_sm) / (ctas > 0 ? ctas : 2) - 1024 - int64_t(fa.sharedSizeBytes);
     int64_t V = (per_cta - int64_t(sm)) / 8 / 256 * 256;
     if (V < 1024) V = 1024;
     const size_t smv = sm + size_t(V) * 8;

@@ -349,6 +349,8 @@ struct BwLayout {
   unsigned o_sm, o_pre, o_lst, o_vals, o_stage, bytes;  // per warp, bytes is a multiple of 16
 };
 
+constexpr unsigned kRecSlot = 264u;  // DENSE: bytes per slot of 8-byte word records (33 records)
+
 __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vmax, int64_t bmax) {
   BwLayout L;
   L.nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
@@ -359,9 +361,10 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
   unsigned off;
   if (mode == MODE_DENSE) {
     L.o_sm = 0;                                  // dir
-    off = (2u * L.nsw + 15u) & ~15u;             // records {bits, rank} per slot word (8 B)
-    L.o_lst = off;
-    off += 256u * L.ns;
+    off = (2u * L.nsw + 15u) & ~15u;             // records {bits, rank} per slot word (8 B),
+    L.o_lst = off;                               // 33 per slot: a stencil's z-neighbour planes
+    off += kRecSlot * L.ns;                      // (same word, other slot) in other banks
+    off = (off + 15u) & ~15u;
     L.o_pre = off;                               // (end of the zeroed region)
     L.o_vals = off;
     off += 8u * (L.nv + 1);  // + scratch
@@ -535,9 +538,9 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         if (in) {
           a.out_col[o + p] = c;
           if (newblk) sh_st_u16(dir + 2u * (d >> 10), (unsigned)(slot + 1));
-          const unsigned wi = unsigned(slot) * 32u + ((d >> 5) & 31);
-          sh_red_or(bits + 8u * wi, 1u << (d & 31));
-          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st(bits + 8u * wi + 4u, (unsigned)p);
+          const unsigned ra = bits + unsigned(slot) * kRecSlot + 8u * ((d >> 5) & 31);
+          sh_red_or(ra, 1u << (d & 31));
+          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st(ra + 4u, (unsigned)p);
         }
         nslot += __popc(nm);
         prevd = __shfl_sync(kFull, d, 31);
@@ -554,8 +557,8 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       unsigned word, base;
       if (MODE == MODE_DENSE) {  // one 8-byte record: the word's bits and its first rank
-        // record (slot-1)*32 + (d>>5)%32: bits - 256 + 256 slot + ((d >> 2) & 0xf8)
-        const uint2 rec = sh_ld_v2(bits - 256u + (sh_ld_u16(dir + 2u * (d >> 10)) << 8) + ((d >> 2) & 0xf8u));
+        // record (d>>5)%32 of slot dir-1: bits + (dir-1)*kRecSlot + ((d >> 2) & 0xf8)
+        const uint2 rec = sh_ld_v2(bits - kRecSlot + sh_ld_u16(dir + 2u * (d >> 10)) * kRecSlot + ((d >> 2) & 0xf8u));
         word = rec.x;
         base = rec.y;
       } else {
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     if (MODE == MODE_FILL) {
       for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
     } else {
-      for (int s = 0; s < nslot; ++s) sh_st(bits + 8u * (unsigned(s) * 32u + lane), 0u);
+      for (int s = 0; s < nslot; ++s) sh_st(bits + unsigned(s) * kRecSlot + 8u * lane, 0u);
       for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
@@ -733,6 +736,9 @@ struct SymLayout {
   int nsw, ns;
   unsigned o_bits, o_stage, bytes;
 };
+// slots of 33 words: the same word of different slots (a stencil's z-neighbour planes) lands in
+// different banks
+constexpr unsigned kSlotBytes = 132u;
 
 __host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
   SymLayout L;
@@ -740,9 +746,25 @@ __host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
   L.nsw = (nwd / 32 + 31) / 32 * 32;
   L.ns = ns;
   L.o_bits = (2u * L.nsw + 15u) & ~15u;
-  L.o_stage = L.o_bits + 128u * (ns + 1);
+  L.o_stage = (L.o_bits + kSlotBytes * (ns + 1) + 15u) & ~15u;
   L.bytes = L.o_stage + 512u;
   return L;
+}
+
+// OR the bit of every active lane into its word (bits of one b_j* step: lanes sharing a word
+// form contiguous runs, the columns being sorted): one shared-memory RED per distinct word —
+// the run's bits are combined by redux.sync over the run's lanes — instead of one per lane
+// (c2: 27 lanes in runs of 3 -> 9 REDs, no same-address serialisation).
+__device__ __forceinline__ void or_runs(unsigned addr, unsigned bit, bool act, unsigned le) {
+  const unsigned prev = __shfl_up_sync(kFull, addr, 1);
+  const bool first = !act || (le == 1u) || prev != addr;
+  const unsigned S = __ballot_sync(kFull, first);
+  const unsigned lo = 31u - __clz(S & le);           // my run's first lane
+  const unsigned after = S & ~le;                    // runs starting after me
+  const unsigned end = after ? __ffs(after) - 1u : 32u;
+  const unsigned mask = (end == 32u ? kFull : ((1u << end) - 1u)) & (kFull << lo);
+  const unsigned v = __reduce_or_sync(mask, act ? bit : 0u);
+  if (first && act) sh_red_or(addr, v);
 }
 
 __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
@@ -756,7 +778,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
   const int32_t* __restrict__ bci = a.B.ci;
   for (unsigned i = lane; i < L.o_stage / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
   __syncwarp();
-  const unsigned lt = lanemask_lt_();
+  const unsigned lt = lanemask_lt_(), le = lt | (1u << lane);
   int bmax = 0;
 
   const int64_t per = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA (L1 reuse)
@@ -813,7 +835,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
                 __syncwarp();
                 if (nd) s1 = sh_ld_u16(dir + 2u * blk);
               }
-              sh_red_or(bits + (s1 << 7) + ((dd >> 3) & 0x7cu), act ? 1u << (dd & 31) : 0u);
+              or_runs(bits + s1 * kSlotBytes + ((dd >> 3) & 0x7cu), 1u << (dd & 31), act && s1 != 0u, le);
             }
           }
           continue;
@@ -843,16 +865,16 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
             }
           }
         }
-        // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: dummy slot)
+        // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: no RED)
 #pragma unroll
         for (int u = 0; u < kGroup; ++u)
-          sh_red_or(bits + (sl[u] << 7) + ((d[u] >> 3) & 0x7cu), sl[u] ? 1u << (d[u] & 31) : 0u);
+          or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le);
       }
     }
     __syncwarp();
     if (nslot > ns) {
       // too many blocks: clear and hand the row to the full-window kernel
-      for (int s = 1; s <= ns; ++s) sh_st(bits + 128u * s + 4u * lane, 0u);
+      for (int s = 1; s <= ns; ++s) sh_st(bits + kSlotBytes * s + 4u * lane, 0u);
       for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
       if (lane == 0) a.bw_ovf_list[atomicAdd(a.bw_ovf_cnt, 1)] = row;
       __syncwarp();
@@ -882,7 +904,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
       while (nzb) {
         const int b = __ffs(nzb) - 1;
         nzb &= nzb - 1;
-        const unsigned wa = bits + (__shfl_sync(kFull, dl, b) << 7) + 4u * lane;
+        const unsigned wa = bits + __shfl_sync(kFull, dl, b) * kSlotBytes + 4u * lane;
         const unsigned word = sh_ld(wa);
         const unsigned nzw = __ballot_sync(kFull, word != 0u);
         if (word) {

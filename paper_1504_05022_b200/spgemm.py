@@ -95,6 +95,47 @@ def partition_rows(u_inclusive_scan, nranks: int):
     return out
 
 
+def _i64(a):
+    import numpy as np
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def dist_block_entries(rp_at_splits):
+    """Host protocol step: entry ranges [(begin, end)] of the row blocks from A.row_ptr at the splits."""
+    import numpy as np
+    x = _i64(rp_at_splits)
+    out = np.zeros(2 * (x.size - 1), dtype=np.int64)
+    check(load().spgemm_dist_block_entries(x.ctypes.data, x.size - 1, out.ctypes.data))
+    return out.reshape(-1, 2)
+
+
+def dist_slice_layout(row_begin, row_end, nnz, k: int):
+    """Host protocol step: global entry offset of every B slice (+ nnz(B) last)."""
+    import numpy as np
+    rb, re_, nz = _i64(row_begin), _i64(row_end), _i64(nnz)
+    out = np.zeros(rb.size + 1, dtype=np.int64)
+    check(load().spgemm_dist_slice_layout(rb.ctypes.data, re_.ctypes.data, nz.ctypes.data, rb.size, k,
+                                          out.ctypes.data))
+    return out
+
+
+def dist_offsets(local_nnz, rank: int):
+    """Host protocol step: (global row-pointer offset of `rank`, nnz(C))."""
+    x = _i64(local_nnz)
+    off, tot = ctypes.c_int64(), ctypes.c_int64()
+    check(load().spgemm_dist_offsets(x.ctypes.data, x.size, rank, ctypes.byref(off), ctypes.byref(tot)))
+    return int(off.value), int(tot.value)
+
+
+def debug_partition(u_scan_dev: torch.Tensor, nranks: int):
+    """The device partition kernel of dist_symbolic on a device inclusive scan (test hook)."""
+    import numpy as np
+    out = np.zeros(nranks + 1, dtype=np.int64)
+    check(load().spgemm_debug_partition(_ptr(u_scan_dev, torch.int64, "scan"), u_scan_dev.numel(), nranks,
+                                        out.ctypes.data))
+    return out
+
+
 class SpGEMM:
     """One C = A·B multiplication: create → symbolic → numeric → destroy (C ABI names)."""
 
@@ -177,16 +218,25 @@ class DistSpGEMM:
     torch.distributed (any backend); all data movement is NCCL inside the library."""
 
     def __init__(self, rank: int, nranks: int, uid: bytes, m: int, k: int, n: int,
-                 A: DeviceCsr | None, B: DeviceCsr | None, flags: int = 0, stream=None):
+                 A: DeviceCsr | None, B: DeviceCsr | None, flags: int = 0, stream=None,
+                 a_rows: tuple | None = None, b_rows: tuple | None = None):
+        """a_rows / b_rows given: sharded inputs (spgemm_dist_create_sharded) — A holds this
+        rank's rows a_rows = (begin, end) of the global A, B this rank's rows b_rows of B."""
         self.lib = load()
         self.A, self.B = A, B
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self.h = ctypes.c_void_p()
         ap = _csr_ptrs(A, "A") if A is not None else (None, None, None)
         bp = _csr_ptrs(B, "B") if B is not None else (None, None, None)
-        check(self.lib.spgemm_dist_create(ctypes.byref(self.h), rank, nranks, uid, m, k, n, ap[0], ap[1], ap[2],
-                                          A.nnz if A is not None else 0, bp[0], bp[1], bp[2],
-                                          B.nnz if B is not None else 0, _stream_handle(self.stream), flags))
+        if a_rows is not None:
+            check(self.lib.spgemm_dist_create_sharded(ctypes.byref(self.h), rank, nranks, uid, m, k, n, a_rows[0],
+                                                      a_rows[1], ap[0], ap[1], ap[2], A.nnz, b_rows[0], b_rows[1],
+                                                      bp[0], bp[1], bp[2], B.nnz, _stream_handle(self.stream),
+                                                      flags))
+        else:
+            check(self.lib.spgemm_dist_create(ctypes.byref(self.h), rank, nranks, uid, m, k, n, ap[0], ap[1], ap[2],
+                                              A.nnz if A is not None else 0, bp[0], bp[1], bp[2],
+                                              B.nnz if B is not None else 0, _stream_handle(self.stream), flags))
         self.n = n
         self.block = None
 
