@@ -168,87 +168,127 @@ def gpu_context(args):
     return ctx
 
 
-def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True):
+def c5_rank_inputs(ctx, scale):
+    """Config 5 at N > 1, generated where it is used (SURVEY §8(e) variant (ii)): this rank's
+    row block of the band A (a balanced split: every interior row has u = 4096) and its row
+    slice of B; the library all-gathers B (spgemm_dist_create_sharded)."""
+    from gen import torchgen as tg
+    world, rank = ctx["world"], ctx["rank"]
+    n = 1 << (scale or 23)
+    r0, r1 = (rank * n) // world, ((rank + 1) * n) // world
+    (arp, aci, aval), _ = tg.band(n, rows=(r0, r1))
+    (brp, bci, bval), _ = tg.uniform_rows(r1 - r0, n, 64, first_row=r0)
+    sg = ctx["sg"]
+    return n, (r0, r1), sg.DeviceCsr(r1 - r0, n, arp, aci, aval), sg.DeviceCsr(r1 - r0, n, brp, bci, bval)
+
+
+def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"):
     """Time `steps` whole-hot-path steps of workload `cfg` (after `warmup`); returns the
-    bench-line fields (value, ms, hbm, roofline, clocks, ...) plus the inputs for e2e."""
+    bench-line fields (value, ms, hbm, roofline, clocks, ...) plus the inputs for e2e.
+    N > 1: variant "i" = inputs replicated on every rank (only the nnz allgather crosses
+    NVLink), "ii" = inputs on rank 0 (partition, A scatter and B broadcast timed inside the
+    step); config 5 at N > 1 always runs as sharded inputs generated per rank."""
     torch, dist, sg = ctx["torch"], ctx["dist"], ctx["sg"]
     world, rank, local = ctx["world"], ctx["rank"], ctx["local"]
     stream, flush, uid = ctx["stream"], ctx["flush"], ctx["uid"]
     flags = sg.FLAG_PRECISE if strategy == "precise" else 0
-    work = make_workload(cfg, args.scale if cfg == args.config else None)
-
-    # inputs resident in HBM
-    dev_inputs = []
-    for name, A, B in work:
-        dA = sg.DeviceCsr.from_host(A)
-        dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
-        dev_inputs.append((name, A, B, dA, dB))
+    c5_dist = cfg == "c5" and world > 1
+    if c5_dist:
+        n5, rows5, dAb5, dBs5 = c5_rank_inputs(ctx, args.scale if cfg == args.config else None)
+        work = [("AB", None, None)]
+        dev_inputs = [("AB", None, None, dAb5, dBs5)]
+    else:
+        work = make_workload(cfg, args.scale if cfg == args.config else None)
+        # inputs resident in HBM
+        dev_inputs = []
+        for name, A, B in work:
+            dA = sg.DeviceCsr.from_host(A)
+            dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
+            dev_inputs.append((name, A, B, dA, dB))
     torch.cuda.synchronize()
 
     dist_ops = {}
 
-    # Row blocks per product.  c5's C (412 GB at n = 2^23) cannot be resident: each rank runs
-    # its rows in waves (C of a wave is freed before the next); the per-rank nnz are still
-    # all-gathered for the global row offsets.  Other configs: one block (dist_* for N > 1).
+    # Row blocks per product.  c5's C (412 GB at n = 2^23) cannot be resident: rows run in
+    # waves (C of a wave is freed before the next) under --wave-gb.  Other configs: one block.
     def plan_blocks(A, Bm):
         m = A.shape[0]
         if cfg != "c5" or Bm is None or isinstance(Bm, str):
             return [(0, m)]
-        r0, r1 = (rank * m) // world, ((rank + 1) * m) // world
-        bl = np.diff(Bm.rp)
-        u_rows = np.zeros(m, dtype=np.int64)
-        np.add.at(u_rows, np.repeat(np.arange(m), np.diff(A.rp)), bl[A.ci])
-        est = 16 * int(u_rows[r0:r1].sum())  # C (12 B) + structure set (4 B) per product
-        budget = int(args.wave_gb * (1 << 30))
-        waves = max(1, -(-est // budget))
-        cuts = [r0 + ((r1 - r0) * w) // waves for w in range(waves + 1)]
+        est = 16 * 4096 * m  # C (12 B) + workspace (~4 B) per product, u = 4096 per row
+        waves = max(1, -(-est // int(args.wave_gb * (1 << 30))))
+        cuts = [(m * w) // waves for w in range(waves + 1)]
         return list(zip(cuts[:-1], cuts[1:]))
 
     blocks_of = {}
-    for (name, A, B, dA, dB) in dev_inputs:
-        blocks_of[name] = plan_blocks(A, A if B is None else B)
-    sharded = cfg == "c5"
+    if c5_dist:
+        m_loc = rows5[1] - rows5[0]
+        est = 16 * 4096 * m_loc
+        waves = torch.tensor([max(1, -(-est // int(args.wave_gb * (1 << 30))))], dtype=torch.int64, device="cuda")
+        dist.all_reduce(waves, op=dist.ReduceOp.MAX)  # every rank runs the same number of collectives
+        W = int(waves.item())
+        cuts = [(m_loc * w) // W for w in range(W + 1)]
+        blocks_of["AB"] = list(zip(cuts[:-1], cuts[1:]))
+    else:
+        for (name, A, B, dA, dB) in dev_inputs:
+            blocks_of[name] = plan_blocks(A, A if B is None else B)
 
     def one_step(collect=False):
         """Whole hot path once: every product of the workload, symbolic + numeric."""
         out = None
         info = []
         for (name, A, B, dA, dB) in dev_inputs:
+            if c5_dist:
+                # sharded inputs: per wave, this rank's A rows and its B slice; the library
+                # all-gathers B, multiplies and stitches the global row offsets
+                for wi, (w0, w1) in enumerate(blocks_of[name]):
+                    blk = sg.DeviceCsr(w1 - w0, dA.cols, dA.rp[w0:w1 + 1], dA.ci, dA.val)
+                    key = ("c5", wi)
+                    op = dist_ops.get(key)
+                    if op is None:
+                        op = sg.DistSpGEMM(rank, world, uid, n5, n5, n5, blk, dB, flags, stream,
+                                           a_rows=(rows5[0] + w0, rows5[0] + w1), b_rows=rows5)
+                        dist_ops[key] = op
+                    rb, re_, ln, gn = op.symbolic()
+                    out = op.numeric()
+                    if collect:
+                        info.append((name, op.stats(), ln, blk, dB))
+                    if len(blocks_of[name]) > 1:
+                        out = None
+                continue
             Bm = dA if dB is None else (out if isinstance(dB, str) else dB)
-            if world == 1 or sharded:
+            if world == 1:
                 blocks = blocks_of[name]
-                tot_nnz = 0
                 for (r0, r1) in blocks:
                     dAb = dA if (r0, r1) == (0, dA.rows) else sg.DeviceCsr(r1 - r0, dA.cols, dA.rp[r0:r1 + 1],
                                                                           dA.ci, dA.val)
                     op = sg.SpGEMM(dAb, Bm, flags, stream)
                     nnz = op.symbolic()
                     out = op.numeric()
-                    tot_nnz += nnz
                     if collect:
                         info.append((name, op.stats(), nnz, dAb, Bm))
                     op.destroy()
                     if len(blocks) > 1:
                         out = None  # capacity-forced waves: the wave's C is released
-                if sharded and world > 1:
-                    # stitching: every rank learns the nnz of all row blocks (global offsets)
-                    t = torch.tensor([tot_nnz], dtype=torch.int64, device="cuda")
-                    allt = [torch.empty_like(t) for _ in range(world)]
-                    with torch.cuda.stream(stream):
-                        dist.all_gather(allt, t)
             else:
                 # the NCCL communicator is created once (outside the timed steps); each step
-                # re-runs the partition, the local four stages and the nnz allgather
-                key = (name, id(Bm))
+                # re-runs the partition, (variant ii: the input movement,) the local four stages
+                # and the nnz allgather
+                key = (name, id(Bm), variant)
                 op = dist_ops.get(key)
                 if op is None:
-                    op = sg.DistSpGEMM(rank, world, uid, dA.rows, dA.cols, Bm.cols, dA, Bm,
-                                       flags | sg.FLAG_INPUTS_REPLICATED, stream)
+                    if variant == "i":
+                        op = sg.DistSpGEMM(rank, world, uid, dA.rows, dA.cols, Bm.cols, dA, Bm,
+                                           flags | sg.FLAG_INPUTS_REPLICATED, stream)
+                    else:
+                        op = sg.DistSpGEMM(rank, world, uid, dA.rows, dA.cols, Bm.cols, dA if rank == 0 else None,
+                                           Bm if rank == 0 else None, flags, stream)
                     dist_ops[key] = op
                 rb, re_, ln, gn = op.symbolic()
                 blk = op.numeric()
                 if collect:
-                    info.append((name, op.stats(), gn, dA, Bm))
+                    info.append((name, op.stats(), ln, sg.DeviceCsr(re_ - rb, dA.cols, dA.rp[rb:re_ + 1], dA.ci,
+                                                                    dA.val), Bm))
                 out = blk  # multi-stage chains on N>1 are not supported (c4 runs at N=1)
         return out, info
 
@@ -298,12 +338,8 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True):
     ms_step = ms_total / steps
 
     # ---------------- per-step accounting (from the collected pass) ----------------
-    sum_u = sum(st["sum_u"] if world == 1 else 0 for _, st, _, _, _ in info)
-    if world > 1:
-        # Σu over the whole problem: every rank sums its local Σu, then all-reduce
-        loc = torch.tensor([sum(st["sum_u"] for _, st, _, _, _ in info)], dtype=torch.int64, device="cuda")
-        dist.all_reduce(loc)
-        sum_u = int(loc.item())
+    # every rank accounts for its own rows (A rows, C rows); B once per product; N > 1: summed
+    sum_u = sum(st["sum_u"] for _, st, _, _, _ in info)
     cb = 0
     nnz_c_tot = 0
     launches = 0
@@ -312,17 +348,15 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True):
         m = dA.rows
         a_nnz = int(dA.rp[-1].item() - dA.rp[0].item()) if m > 0 else 0  # a row block's own entries
         cb += csr_bytes(m, a_nnz) + csr_bytes(m, nnz_c)
-        if (name, id(Bm)) not in seen_b:  # B is read once per product even across waves
-            cb += csr_bytes(Bm.rows, Bm.nnz)
+        if (name, id(Bm)) not in seen_b and rank == 0:  # B is read once per product even across waves
+            cb += csr_bytes(n5 if c5_dist else Bm.rows, (int(st["nnz_b"]) if c5_dist else Bm.nnz))
             seen_b.add((name, id(Bm)))
         nnz_c_tot += nnz_c
         launches += st["launches_symbolic"] + st["launches_numeric"]
-    if sharded and world > 1:
-        t = torch.tensor([nnz_c_tot, cb - sum(csr_bytes(d[4].rows, d[4].nnz) for d in info[:1])],
-                         dtype=torch.int64, device="cuda")
+    if world > 1:
+        t = torch.tensor([sum_u, nnz_c_tot, cb], dtype=torch.int64, device="cuda")
         dist.all_reduce(t)
-        nnz_c_tot = int(t[0].item())
-        cb = int(t[1].item()) + csr_bytes(info[0][4].rows, info[0][4].nnz)
+        sum_u, nnz_c_tot, cb = (int(x) for x in t.tolist())
     gflops = 2.0 * sum_u / (ms_step * 1e-3) / 1e9
     peaks = {}
     try:
@@ -387,7 +421,10 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True):
         "config": {"workload": "%s: %s" % (cfg, CONFIGS[cfg]),
                    "strategy": strategy, "sum_u": sum_u, "nnz_c": nnz_c_tot,
                    "nnz_a": int(sum(d[3].nnz for d in dev_inputs)),
-                   "parallelism": "row blocks x%d (dist_* ABI, NCCL)" % world if world > 1 else "1 GPU",
+                   "parallelism": ("row blocks x%d (dist_* ABI, NCCL), variant %s" % (
+                       world, "ii: sharded inputs generated per rank, B all-gathered" if c5_dist else
+                       ("i: inputs replicated" if variant == "i" else "ii: inputs on rank 0"))) if world > 1
+                   else "1 GPU",
                    "l2": "flushed before every timed step (512 MiB memset, outside the timed window)",
                    "waves": {n: len(b) for n, b in blocks_of.items() if len(b) > 1} or None,
                    "scale": args.scale if cfg == args.config else None},
@@ -421,6 +458,11 @@ def run_gpu(args):
     torch, dist, sg = ctx["torch"], ctx["dist"], ctx["sg"]
     world, rank = ctx["world"], ctx["rank"]
     result, aux = measure(args, ctx, args.config, args.strategy, args.steps, args.warmup)
+    if world > 1 and args.config != "c5" and not args.no_variant_ii:
+        # SURVEY §8(e) variant (ii): the same step with the inputs on rank 0 only
+        r2, _ = measure(args, ctx, args.config, args.strategy, args.steps, args.warmup, variant="ii")
+        result["variant_ii"] = {"value": r2["value"], "unit": "GFlop/s", "ms_per_step": r2["ms_per_step"],
+                                "parallelism": r2["config"]["parallelism"]}
     # ---------------- end-to-end through the public API with host buffers ----------------
     if aux["can_e2e"] and not args.no_e2e:
         result["e2e"] = e2e_measure(args, aux["work"], aux["flags"], ctx["stream"], aux["sum_u"])
@@ -651,6 +693,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--wave-gb", type=float, default=80.0, help="c5: device memory budget per row wave")
     ap.add_argument("--no-per-config", action="store_true", help="skip the per_config block (other configs)")
+    ap.add_argument("--no-variant-ii", action="store_true", help="N > 1: skip the inputs-on-rank-0 variant")
     ap.add_argument("--per-config-steps", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -78,15 +78,16 @@ def band(n: int, lo: int = 32, hi: int = 31, mode: str = "real", seed: int = SEE
 
 
 def uniform_rows(n_rows: int, n_cols: int, r: int = 64, seed: int = SEED + 1, mode: str = "real",
-                 vseed: int = SEED + 4, device="cuda", chunk: int = 1 << 20):
-    """gen.uniform_rows on `device` (rows with a collision redraw from further counters)."""
+                 vseed: int = SEED + 4, device="cuda", chunk: int = 1 << 20, first_row: int = 0):
+    """gen.uniform_rows on `device` (rows with a collision redraw from further counters).
+    first_row > 0: rows [first_row, first_row + n_rows) of the same matrix (a rank's slice)."""
     rp = torch.arange(n_rows + 1, dtype=torch.int64, device=device) * r
     ci = torch.empty(n_rows * r, dtype=torch.int32, device=device)
     val = torch.empty(n_rows * r, dtype=torch.float64, device=device)
     t = torch.arange(r, dtype=torch.int64, device=device)
     for r0 in range(0, n_rows, chunk):
         r1 = min(n_rows, r0 + chunk)
-        rows = torch.arange(r0, r1, dtype=torch.int64, device=device)
+        rows = torch.arange(first_row + r0, first_row + r1, dtype=torch.int64, device=device)
         h = hash3(seed, rows[:, None], t[None, :])
         cols = _srl(h, 0)  # bit pattern
         # uint64 modulo n_cols: split into high/low 32-bit halves (exact in int64)
@@ -100,7 +101,7 @@ def uniform_rows(n_rows: int, n_cols: int, r: int = 64, seed: int = SEED + 1, mo
         if bad:
             cols_cpu = cols.cpu()
             for b in bad:
-                i = r0 + b
+                i = first_row + r0 + b
                 got = list(dict.fromkeys(cols_cpu[b].tolist()))
                 tt = r
                 while len(got) < r:

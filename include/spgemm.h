@@ -80,7 +80,7 @@ typedef struct spgemm_stats {
   int64_t long_entries;     /* final long-row arena capacity in entries                     */
   int32_t growth_rounds;    /* re-allocation rounds of the long-row path ("2x each time" [P:297]) */
   int32_t flags;
-  int64_t workspace_bytes;  /* device bytes held by the handle after symbolic               */
+  int64_t workspace_bytes;  /* device bytes held by the handle after symbolic (pool + mapped long-row arena) */
   float stage_ms[4];        /* CUDA-event times on the handle's stream: symbolic stage 1+2,
                                stage 3 (all classes incl. long rows), stage-4 scan; numeric  */
   float tier_ms[SPGEMM_NUM_TIERS];         /* stage-3 time per class (last symbolic;

@@ -749,7 +749,7 @@ spgemm_status_t spgemm_get_stats(spgemm_handle_t h, spgemm_stats_t* out) {
   out->long_entries = h->long_entries;
   out->growth_rounds = h->growth_rounds;
   out->flags = (int32_t)h->flags;
-  out->workspace_bytes = (int64_t)h->bytes;
+  out->workspace_bytes = (int64_t)(h->bytes + h->arena_col.mapped + h->arena_val.mapped);
   if (h->sym_ok && h->ev_ok) {
     cudaEventSynchronize(h->ev[3]);
     cudaEventElapsedTime(&out->stage_ms[0], h->ev[0], h->ev[1]);

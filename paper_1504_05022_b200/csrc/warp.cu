@@ -751,20 +751,21 @@ __host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
   return L;
 }
 
-// OR the bit of every active lane into its word (bits of one b_j* step: lanes sharing a word
-// form contiguous runs, the columns being sorted): one shared-memory RED per distinct word —
-// the run's bits are combined by redux.sync over the run's lanes — instead of one per lane
-// (c2: 27 lanes in runs of 3 -> 9 REDs, no same-address serialisation).
-__device__ __forceinline__ void or_runs(unsigned addr, unsigned bit, bool act, unsigned le) {
-  const unsigned prev = __shfl_up_sync(kFull, addr, 1);
-  const bool first = !act || (le == 1u) || prev != addr;
-  const unsigned S = __ballot_sync(kFull, first);
-  const unsigned lo = 31u - __clz(S & le);           // my run's first lane
-  const unsigned after = S & ~le;                    // runs starting after me
-  const unsigned end = after ? __ffs(after) - 1u : 32u;
-  const unsigned mask = (end == 32u ? kFull : ((1u << end) - 1u)) & (kFull << lo);
-  const unsigned v = __reduce_or_sync(mask, act ? bit : 0u);
-  if (first && act) sh_red_or(addr, v);
+// OR the bit of every active lane into its word (the lanes of one b_j* step hold sorted
+// columns, so lanes sharing a word form contiguous runs): the bits of up to four consecutive
+// lanes of a run are combined with two shuffles and one lane of each group of four issues the
+// RED — c2's runs of three cost one RED instead of three same-address ones.
+__device__ __forceinline__ void or_runs(unsigned addr, unsigned bit, bool act, unsigned le, int lane) {
+  const unsigned key = act ? addr : 0xffffffe0u + lane;  // idle lanes: unique, never shared
+  unsigned v = act ? bit : 0u;
+  const unsigned k1 = __shfl_down_sync(kFull, key, 1), v1 = __shfl_down_sync(kFull, v, 1);
+  if (k1 == key && lane < 31) v |= v1;
+  const unsigned k2 = __shfl_down_sync(kFull, key, 2), v2 = __shfl_down_sync(kFull, v, 2);
+  if (k2 == key && lane < 30) v |= v2;
+  const unsigned kp = __shfl_up_sync(kFull, key, 1);
+  const unsigned S = __ballot_sync(kFull, lane == 0 || kp != key);  // run starts
+  const unsigned pos = lane - (31u - __clz(S & le));                // position in the run
+  if (act && (pos & 3u) == 0u) sh_red_or(addr, v);
 }
 
 __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
@@ -835,7 +836,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
                 __syncwarp();
                 if (nd) s1 = sh_ld_u16(dir + 2u * blk);
               }
-              or_runs(bits + s1 * kSlotBytes + ((dd >> 3) & 0x7cu), 1u << (dd & 31), act && s1 != 0u, le);
+              or_runs(bits + s1 * kSlotBytes + ((dd >> 3) & 0x7cu), 1u << (dd & 31), act && s1 != 0u, le, lane);
             }
           }
           continue;
@@ -868,7 +869,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
         // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: no RED)
 #pragma unroll
         for (int u = 0; u < kGroup; ++u)
-          or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le);
+          or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le, lane);
       }
     }
     __syncwarp();

@@ -10,7 +10,7 @@ if [ -n "$K" ]; then
 fi
 for c in ${BENCH_CFGS:-}; do
   for s in ${STRATS:-precise}; do
-    timeout 600 python bench.py --config $c --strategy $s --no-e2e --no-cpu --steps 5 > $OUT/b_${c}_$s.json 2> $OUT/b_${c}_$s.err
+    timeout 600 python bench.py --config $c --strategy $s --no-e2e --no-cpu --no-per-config --steps 5 > $OUT/b_${c}_$s.json 2> $OUT/b_${c}_$s.err
     python -c "
 import json; d=json.load(open('$OUT/b_${c}_$s.json')); print('$c $s', d['ms_per_step'], d['value'], {k: [round(x,2) for x in v] for k,v in d['stage_ms'].items()}, d['roofline']['kernel'], d['roofline']['launch_ms'])" || tail -3 $OUT/b_${c}_$s.err
   done
