@@ -38,6 +38,16 @@ CONFIGS = {
     "c4a": "Galerkin R·(A·P), A = 3D 7-point 256³, tentative 2×2×2 aggregation P",
     "c4b": "Galerkin R·(A·P), A = 3D 7-point 256³, Jacobi-smoothed aggregation P (ω=3/4)",
     "c5": "C = A·B, A = band(64) n=2^23, B = 64 uniform columns per row",
+    # the paper's Galerkin set ([P:393-397]): AMG hierarchies (3 levels) of
+    # smoothed aggregation with a Jacobi smoother; every level's P^T(AP) (suffix _ptap: (P^T A)P)
+    "g2d5": "Galerkin P^T(AP), 3-level AMG, 2D 5-point Poisson 1024x1024",
+    "g2d9": "Galerkin P^T(AP), 3-level AMG, 2D 9-point Poisson 1024x1024",
+    "g3d7": "Galerkin P^T(AP), 3-level AMG, 3D 7-point Poisson 101^3",
+    "g3d27": "Galerkin P^T(AP), 3-level AMG, 3D 27-point Poisson 101^3",
+    "g2d5_ptap": "Galerkin (P^T A)P, 3-level AMG, 2D 5-point Poisson 1024x1024",
+    "g2d9_ptap": "Galerkin (P^T A)P, 3-level AMG, 2D 9-point Poisson 1024x1024",
+    "g3d7_ptap": "Galerkin (P^T A)P, 3-level AMG, 3D 7-point Poisson 101^3",
+    "g3d27_ptap": "Galerkin (P^T A)P, 3-level AMG, 3D 27-point Poisson 101^3",
 }
 SMI_REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
                "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown", "display_clock_setting"]
@@ -77,6 +87,16 @@ def make_workload(cfg: str, scale: int | None = None):
         P = gen.aggregation_P(n, smoothed=(cfg == "c4b"))
         R = gen.transpose(P)
         return [("AP", A, P), ("R(AP)", R, "prev")]
+    if cfg.startswith("g"):
+        kind = cfg[1:].split("_")[0]
+        n = scale or (1024 if kind.startswith("2d") else 101)
+        prods = []
+        for lvl, (A, P, R) in enumerate(gen.amg_levels(kind, n, 3)):
+            if cfg.endswith("_ptap"):   # (P^T A) P
+                prods += [("RA%d" % lvl, R, A), ("(RA)P%d" % lvl, "prev", P)]
+            else:                       # P^T (A P)
+                prods += [("AP%d" % lvl, A, P), ("R(AP)%d" % lvl, R, "prev")]
+        return prods
     if cfg == "c5":
         n = 1 << (scale or 23)
         if tg is not None:
@@ -202,7 +222,7 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
         # inputs resident in HBM
         dev_inputs = []
         for name, A, B in work:
-            dA = sg.DeviceCsr.from_host(A)
+            dA = "prev" if isinstance(A, str) else sg.DeviceCsr.from_host(A)
             dB = None if B is None else ("prev" if isinstance(B, str) else sg.DeviceCsr.from_host(B))
             dev_inputs.append((name, A, B, dA, dB))
     torch.cuda.synchronize()
@@ -212,9 +232,9 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
     # Row blocks per product.  c5's C (412 GB at n = 2^23) cannot be resident: rows run in
     # waves (C of a wave is freed before the next) under --wave-gb.  Other configs: one block.
     def plan_blocks(A, Bm):
+        if cfg != "c5" or isinstance(A, str) or Bm is None or isinstance(Bm, str):
+            return [(0, None)]  # one block: the whole product
         m = A.shape[0]
-        if cfg != "c5" or Bm is None or isinstance(Bm, str):
-            return [(0, m)]
         est = 16 * 4096 * m  # C (12 B) + workspace (~4 B) per product, u = 4096 per row
         waves = max(1, -(-est // int(args.wave_gb * (1 << 30))))
         cuts = [(m * w) // waves for w in range(waves + 1)]
@@ -256,12 +276,14 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
                     if len(blocks_of[name]) > 1:
                         out = None
                 continue
+            if isinstance(dA, str):
+                dA = out  # chained product: the previous C is this A
             Bm = dA if dB is None else (out if isinstance(dB, str) else dB)
             if world == 1:
                 blocks = blocks_of[name]
                 for (r0, r1) in blocks:
-                    dAb = dA if (r0, r1) == (0, dA.rows) else sg.DeviceCsr(r1 - r0, dA.cols, dA.rp[r0:r1 + 1],
-                                                                          dA.ci, dA.val)
+                    dAb = dA if r1 is None or (r0, r1) == (0, dA.rows) else \
+                        sg.DeviceCsr(r1 - r0, dA.cols, dA.rp[r0:r1 + 1], dA.ci, dA.val)
                     op = sg.SpGEMM(dAb, Bm, flags, stream)
                     nnz = op.symbolic()
                     out = op.numeric()
@@ -420,7 +442,7 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
                                                             else "real values"),
         "config": {"workload": "%s: %s" % (cfg, CONFIGS[cfg]),
                    "strategy": strategy, "sum_u": sum_u, "nnz_c": nnz_c_tot,
-                   "nnz_a": int(sum(d[3].nnz for d in dev_inputs)),
+                   "nnz_a": int(sum(d[3].nnz for d in dev_inputs if not isinstance(d[3], str))),
                    "parallelism": ("row blocks x%d (dist_* ABI, NCCL), variant %s" % (
                        world, "ii: sharded inputs generated per rank, B all-gathered" if c5_dist else
                        ("i: inputs replicated" if variant == "i" else "ii: inputs on rank 0"))) if world > 1
@@ -450,7 +472,7 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
     return result, dict(work=work, flags=flags, sum_u=sum_u, can_e2e=can_e2e)
 
 
-PER_CONFIG = ["c2", "c3a", "c3b", "c4a", "c4b"]
+PER_CONFIG = ["c2", "c3a", "c3b", "c4a", "c4b", "g2d5", "g2d9", "g3d7", "g3d27", "g3d27_ptap"]
 
 
 def run_gpu(args):
@@ -509,8 +531,10 @@ def e2e_measure(args, work, flags, stream, sum_u):
     host = []
     h2d = 0
     for name, A, B in work:
-        hA = (pin(A.rp, torch.int64), pin(A.ci, torch.int32), pin(A.val, torch.float64), A.shape)
-        h2d += csr_bytes(A.shape[0], A.nnz)
+        hA = None
+        if not isinstance(A, str):
+            hA = (pin(A.rp, torch.int64), pin(A.ci, torch.int32), pin(A.val, torch.float64), A.shape)
+            h2d += csr_bytes(A.shape[0], A.nnz)
         hB = None
         if B is not None and not isinstance(B, str):
             hB = (pin(B.rp, torch.int64), pin(B.ci, torch.int32), pin(B.val, torch.float64), B.shape)
@@ -528,7 +552,7 @@ def e2e_measure(args, work, flags, stream, sum_u):
         out = None
         d2h = 0
         for hA, hB, B in host:
-            dA = todev(hA)
+            dA = out if hA is None else todev(hA)
             dB = dA if B is None else (out if isinstance(B, str) else todev(hB))
             op = sg.SpGEMM(dA, dB, flags, stream)
             nnz = op.symbolic()

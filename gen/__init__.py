@@ -310,6 +310,53 @@ def aggregation_P(n: int, smoothed: bool = False) -> Csr:
     return Csr((N, h ** 3), rp, out_c[valid].astype(np.int32), out_v[valid])
 
 
+def _to_scipy(M: Csr):
+    import scipy.sparse as sp
+    return sp.csr_matrix((M.val, M.ci.astype(np.int64), M.rp), shape=M.shape)
+
+
+def _from_scipy(S) -> Csr:
+    S = S.tocsr()
+    S.sum_duplicates()
+    S.sort_indices()
+    return Csr(S.shape, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data.astype(np.float64))
+
+
+def amg_levels(kind: str, n: int, levels: int = 3, omega: float = 0.75):
+    """The paper's Galerkin workload ([P:393-397]): an AMG hierarchy of a Poisson problem with
+    smoothed aggregation and a Jacobi smoother.  Level 0: A = stencil(kind, n) (2D 5/9-point
+    on n², 3D 7/27-point on n³).  Each level aggregates 2 (2D: 2×2, 3D: 2×2×2) neighbouring
+    grid points of the level's grid (ceil(n/2) points per axis; odd n leaves boundary
+    aggregates of one point), P_t[i, agg(i)] = 1, P = (I − ω D⁻¹ A)·P_t (Jacobi smoothing,
+    ω = 3/4: reading Q15), R = Pᵀ, and the next level's operator is A' = R·A·P.
+    Returns [(A_l, P_l, R_l)] for l < levels.  Input construction only (scipy.sparse); the
+    products the benchmark and tests run on these inputs go through libspgemm / the oracle.
+    Stored zeros from exact cancellation are dropped by scipy (any valid CSR is an input)."""
+    import scipy.sparse as sp
+    dim = _STENCILS[kind][0]
+    A = _to_scipy(stencil(kind, n))
+    out = []
+    g = n
+    for _ in range(levels):
+        h = (g + 1) // 2
+        N = g ** dim
+        idx = np.arange(N, dtype=np.int64)
+        x, y = idx % g, (idx // g) % g
+        if dim == 2:
+            agg = (y >> 1) * h + (x >> 1)
+        else:
+            z = idx // (g * g)
+            agg = ((z >> 1) * h + (y >> 1)) * h + (x >> 1)
+        Pt = sp.csr_matrix((np.ones(N), agg, np.arange(N + 1)), shape=(N, h ** dim))
+        Dinv = sp.diags(1.0 / A.diagonal())
+        P = (Pt - omega * (Dinv @ (A @ Pt))).tocsr()
+        R = P.T.tocsr()
+        out.append((_from_scipy(A), _from_scipy(P), _from_scipy(R)))
+        A = (R @ (A @ P)).tocsr()
+        g = h
+    return out
+
+
 def transpose(M: Csr) -> Csr:
     """Rᵀ materialisation (stable: rows of the transpose keep ascending columns)."""
     m, n = M.shape

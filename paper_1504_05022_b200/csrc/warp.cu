@@ -285,51 +285,55 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 //          is written in order with no sort (precise numeric into C, hybrid into C~)
 // The bitmap is zero between rows: every row clears the words it set.
 // 32-bit shared-window addressing (the per-warp regions are carved from dynamic shared memory;
-// explicit ld/st/atom.shared keep every access a direct LDS/STS/ATOMS).
+// explicit ld/st/atom.shared keep every access a direct LDS/STS/ATOMS).  The helpers are volatile
+// asm WITHOUT a memory clobber: their order among themselves is kept (volatile), while the
+// read-only global gathers of B (__ldg) may be scheduled across them — the next steps' loads
+// are in flight while the current step's shared-memory work runs.  Lane-to-lane hand-offs
+// through shared memory are fenced by __syncwarp().
 __device__ __forceinline__ unsigned sh_atom_or(unsigned addr, unsigned v) {
   unsigned r;
-  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v));
   return r;
 }
 __device__ __forceinline__ void sh_red_or(unsigned addr, unsigned v) {
-  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 __device__ __forceinline__ unsigned sh_ld(unsigned addr) {
   unsigned r;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr) : "memory");
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
   return r;
 }
 __device__ __forceinline__ void sh_st(unsigned addr, unsigned v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 __device__ __forceinline__ unsigned sh_ld_u16(unsigned addr) {
   unsigned short r;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr) : "memory");
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr));
   return r;
 }
 __device__ __forceinline__ void sh_st_u16(unsigned addr, unsigned v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
 }
 __device__ __forceinline__ double sh_ld_f64(unsigned addr) {
   double r;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(addr) : "memory");
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(addr));
   return r;
 }
 __device__ __forceinline__ void sh_st_f64(unsigned addr, double v) {
-  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v));
 }
 __device__ __forceinline__ int4 sh_ld_v4(unsigned addr) {
   int4 r;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
   return r;
 }
 __device__ __forceinline__ uint2 sh_ld_v2(unsigned addr) {
   uint2 r;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr) : "memory");
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
   return r;
 }
 __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u));
 }
 
 // Per-warp shared-memory layout of the window class (byte offsets from the warp's base).
@@ -735,6 +739,7 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
 struct SymLayout {
   int nsw, ns;
   unsigned o_bits, o_stage, bytes;
+  int combine;  // combine the bits of a run's lanes before the RED (or_runs)
 };
 // slots of 33 words: the same word of different slots (a stencil's z-neighbour planes) lands in
 // different banks
@@ -836,7 +841,7 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
                 __syncwarp();
                 if (nd) s1 = sh_ld_u16(dir + 2u * blk);
               }
-              or_runs(bits + s1 * kSlotBytes + ((dd >> 3) & 0x7cu), 1u << (dd & 31), act && s1 != 0u, le, lane);
+              sh_red_or(bits + s1 * kSlotBytes + ((dd >> 3) & 0x7cu), act ? 1u << (dd & 31) : 0u);
             }
           }
           continue;
@@ -867,9 +872,15 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
           }
         }
         // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: no RED)
+        if (L.combine) {
 #pragma unroll
-        for (int u = 0; u < kGroup; ++u)
-          or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le, lane);
+          for (int u = 0; u < kGroup; ++u)
+            or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le, lane);
+        } else {
+#pragma unroll
+          for (int u = 0; u < kGroup; ++u)  // idle lanes and slot-less rows: OR 0 into the dummy slot
+            sh_red_or(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), sl[u] ? 1u << (d[u] & 31) : 0u);
+        }
       }
     }
     __syncwarp();
@@ -1035,7 +1046,9 @@ static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
 }
 
 static cudaError_t launch_sym(const Stage3Args& a, cudaStream_t s) {
-  const SymLayout L = sym_layout(a.bw_wmax, kBs2Slots);
+  SymLayout L = sym_layout(a.bw_wmax, kBs2Slots);
+  static const int combine = getenv("SPGEMM_SYM_COMBINE") ? atoi(getenv("SPGEMM_SYM_COMBINE")) : 0;
+  L.combine = combine;
   constexpr int nw = 8;
   const size_t bytes = size_t(nw) * L.bytes;
   cudaError_t e = cudaFuncSetAttribute(k_bw_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
