@@ -608,7 +608,8 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
     const int64_t per_cta = int64_t(smem_sm) / (ctas > 0 ? ctas : 2) - 1024 - int64_t(fa.sharedSizeBytes);
     int64_t V = (per_cta - int64_t(sm)) / 8 / 256 * 256;
     if (V < 1024) V = 1024;
-    static const int use_smem = getenv("SPGEMM_RANK_SMEM") ? atoi(getenv("SPGEMM_RANK_SMEM")) : 1;
+    // shared accumulation for tiles of at most V entries measured slower on c3b (70 vs 51 ms)
+    static const int use_smem = getenv("SPGEMM_RANK_SMEM") ? atoi(getenv("SPGEMM_RANK_SMEM")) : 0;
     if (!use_smem) V = 0;  // every tile accumulates in place in the output (L2)
     const size_t smv = sm + size_t(V) * 8;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);

@@ -539,12 +539,24 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         const bool newblk = in && (dp < 0 || (dp >> 10) != (d >> 10));
         const unsigned nm = __ballot_sync(kFull, newblk);
         const int slot = nslot + __popc(nm & (lanemask_lt_() | (1u << lane))) - 1;
+        // the bits of a word's lanes (contiguous: the set is sorted) are ORed together first,
+        // so each word takes one RED (same-address REDs serialise: 7.6x the ideal wavefronts)
+        const int wkey = in ? (d >> 5) : -1 - lane;
+        unsigned wbits = in ? 1u << (d & 31) : 0u;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const unsigned vo = __shfl_down_sync(kFull, wbits, sh);
+          const int ko = __shfl_down_sync(kFull, wkey, sh);
+          if (lane + sh < 32 && ko == wkey) wbits |= vo;
+        }
+        const bool wfirst = dp < 0 || (dp >> 5) != (d >> 5);  // first entry of its word overall
+        const int kprev = __shfl_up_sync(kFull, wkey, 1);
         if (in) {
           a.out_col[o + p] = c;
           if (newblk) sh_st_u16(dir + 2u * (d >> 10), (unsigned)(slot + 1));
           const unsigned ra = bits + unsigned(slot) * kRecSlot + 8u * ((d >> 5) & 31);
-          sh_red_or(ra, 1u << (d & 31));
-          if (dp < 0 || (dp >> 5) != (d >> 5)) sh_st(ra + 4u, (unsigned)p);
+          if (lane == 0 || kprev != wkey) sh_red_or(ra, wbits);  // first lane of its run here
+          if (wfirst) sh_st(ra + 4u, (unsigned)p);
         }
         nslot += __popc(nm);
         prevd = __shfl_sync(kFull, d, 31);
