@@ -62,8 +62,9 @@ enum {
                                               a structure-only stage 3 and numeric recomputes the
                                               rows straight into C (no temporary C~).  Default is
                                               the paper's hybrid method ([P:224]): C~ + stage-4 copy */
-  SPGEMM_FLAG_UPPER_BOUND = 1u << 3        /* hybrid with the upper-bound allocation for long rows
+  SPGEMM_FLAG_UPPER_BOUND = 1u << 3,       /* hybrid with the upper-bound allocation for long rows
                                               too (C~ row = min(u_i, n), no growth) [P:169]        */
+  SPGEMM_FLAG_FP32 = 1u << 4               /* SpSGEMM: fp32 values (set by spgemm_create_f32)       */
 };
 
 /* Number of stage-2 size classes ("bins", re-derived for 228 KB smem/SM). */
@@ -117,6 +118,20 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t handle, int64_t* c_nnz);
  * (no successful symbolic), INVALID_VALUE, CUDA. */
 spgemm_status_t spgemm_numeric(spgemm_handle_t handle, int64_t* c_row_ptr, int32_t* c_col_idx,
                                double* c_val);
+
+/* SpSGEMM — the paper's single-precision runs ([P:403], [P:663]): the same four stages with
+ * fp32 values (float a_val / b_val / c_val, DEVICE pointers); every product a_ij·b_jk is
+ * rounded to fp32 and the sums run in fp32 in the same j-ascending order as the fp64 path.
+ * Structure, row pointers and errors are those of spgemm_create / spgemm_numeric; the handle
+ * must be finished with spgemm_numeric_f32 (spgemm_numeric on it fails with INVALID_VALUE,
+ * and spgemm_numeric_f32 on an fp64 handle likewise).  Not available through dist_*. */
+spgemm_status_t spgemm_create_f32(spgemm_handle_t* handle, int64_t m, int64_t k, int64_t n,
+                                  const int64_t* a_row_ptr, const int32_t* a_col_idx,
+                                  const float* a_val, int64_t a_nnz, const int64_t* b_row_ptr,
+                                  const int32_t* b_col_idx, const float* b_val, int64_t b_nnz,
+                                  spgemm_stream_t stream, uint32_t flags);
+spgemm_status_t spgemm_numeric_f32(spgemm_handle_t handle, int64_t* c_row_ptr, int32_t* c_col_idx,
+                                   float* c_val);
 
 /* Frees all workspace.  NULL → no-op.  Synchronises the handle's stream. */
 spgemm_status_t spgemm_destroy(spgemm_handle_t handle);

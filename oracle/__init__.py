@@ -62,6 +62,10 @@ def _load():
         lib.oracle_spgemm_fill.restype = None
         lib.oracle_spgemm_fill.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, I64P, I32P, F64P,
                                            I64P, I32P, F64P, I64P, I32P, F64P, F64P, ctypes.c_int]
+        F32P = ctypes.POINTER(ctypes.c_float)
+        lib.oracle_spgemm_fill_f32.restype = None
+        lib.oracle_spgemm_fill_f32.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, I64P, I32P, F32P,
+                                               I64P, I32P, F32P, I64P, I32P, F32P, F64P, ctypes.c_int]
         lib.oracle_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -121,8 +125,10 @@ class OracleResult:
 
 
 def spgemm(A, B, r0: int = 0, r1: int | None = None, with_bound: bool = True,
-           threads: int = 0) -> OracleResult:
-    """C[r0:r1] = A[r0:r1]·B by row-wise Gustavson + dense SPA [P:115-138], [P:142]."""
+           threads: int = 0, fp32: bool = False) -> OracleResult:
+    """C[r0:r1] = A[r0:r1]·B by row-wise Gustavson + dense SPA [P:115-138], [P:142].
+    fp32: SpSGEMM — A's and B's values taken as float32, products and sums in float32
+    (the result's val is float32)."""
     if A.shape[1] != B.shape[0]:
         raise ValueError("dimension mismatch: A is %dx%d, B is %dx%d" % (A.shape + B.shape))
     m, n = A.shape[0], B.shape[1]
@@ -138,8 +144,17 @@ def spgemm(A, B, r0: int = 0, r1: int | None = None, with_bound: bool = True,
     np.cumsum(nnz_row, out=crp[1:])
     nnz = int(crp[-1])
     cci = np.empty(nnz, dtype=np.int32)
-    cval = np.empty(nnz, dtype=np.float64)
     bound = np.empty(nnz, dtype=np.float64) if with_bound else None
+    if fp32:
+        F32P = ctypes.POINTER(ctypes.c_float)
+        a32 = np.ascontiguousarray(A.val, dtype=np.float32)
+        b32 = np.ascontiguousarray(B.val, dtype=np.float32)
+        cval = np.empty(nnz, dtype=np.float32)
+        lib.oracle_spgemm_fill_f32(r0, r1, n, _p(arp, I64P), _p(aci, I32P), _p(a32, F32P), _p(brp, I64P),
+                                   _p(bci, I32P), _p(b32, F32P), _p(crp, I64P), _p(cci, I32P), _p(cval, F32P),
+                                   _p(bound, F64P) if bound is not None else None, threads)
+        return OracleResult(crp, cci, cval, bound, r0)
+    cval = np.empty(nnz, dtype=np.float64)
     lib.oracle_spgemm_fill(r0, r1, n, _p(arp, I64P), _p(aci, I32P), _p(aval, F64P), _p(brp, I64P),
                            _p(bci, I32P), _p(bval, F64P), _p(crp, I64P), _p(cci, I32P), _p(cval, F64P),
                            _p(bound, F64P) if bound is not None else None, threads)

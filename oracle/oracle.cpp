@@ -20,6 +20,8 @@
  *                          al. cited at [P:142].  Rows come out sorted and duplicate-
  *                          free (CSR, [P:113]); no numeric dropping ("does not take into
  *                          consideration cancellation" [P:169]).
+ *   - oracle_spgemm_fill_f32: the same fill in single precision (SpSGEMM, the paper's SP
+ *                          experiments [P:403], [P:663]).
  *   - oracle_validate_csr: the CSR invariants the paper assumes (sorted columns, the
  *                          footnote at [P:178]).
  *
@@ -172,6 +174,58 @@ void oracle_spgemm_fill(int64_t r0, int64_t r1, int64_t n, const int64_t* a_rp,
           } else {
             acc[c] = acc[c] + prod;                    /* line 11: accumulate       */
             if (bound) absacc[c] = absacc[c] + std::fabs(a) * std::fabs(b_val[q]);
+          }
+        }
+      }
+      std::sort(list.begin(), list.end());             /* CSR: ascending columns   */
+      int64_t base = c_rp[i - r0];
+      for (size_t t = 0; t < list.size(); ++t) {
+        c_ci[base + (int64_t)t] = list[t];
+        c_val[base + (int64_t)t] = acc[list[t]];
+        if (bound) bound[base + (int64_t)t] = absacc[list[t]];
+      }
+    }
+  }
+}
+
+/* ---- SpSGEMM fill (the paper's single-precision runs, [P:403], [P:663]) ------------
+   The same algorithm as oracle_spgemm_fill in IEEE single precision: the product a_ij·b_jk
+   is rounded to float (line 6), the first product of an entry initialises it (line 9),
+   later ones are added in float (line 11), in the fixed order j ascending, then column
+   ascending.  Bound (double) = sum of |a_ij|·|b_jk| for the tolerance check. */
+void oracle_spgemm_fill_f32(int64_t r0, int64_t r1, int64_t n, const int64_t* a_rp,
+                            const int32_t* a_ci, const float* a_val, const int64_t* b_rp,
+                            const int32_t* b_ci, const float* b_val, const int64_t* c_rp,
+                            int32_t* c_ci, float* c_val, double* bound, int threads) {
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel num_threads(threads)
+#endif
+  {
+    size_t nn = (size_t)std::max<int64_t>(n, 1);
+    std::vector<float> acc(nn);
+    std::vector<double> absacc(bound ? nn : 1);
+    std::vector<int64_t> mark(nn, -1);
+    std::vector<int32_t> list;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 256)
+#endif
+    for (int64_t i = r0; i < r1; ++i) {
+      list.clear();                                    /* line 2: c_i* <- empty     */
+      for (int64_t p = a_rp[i]; p < a_rp[i + 1]; ++p) { /* line 3: each a_ij        */
+        int64_t j = a_ci[p];
+        float a = a_val[p];
+        for (int64_t q = b_rp[j]; q < b_rp[j + 1]; ++q) { /* line 5: each b_jk     */
+          int32_t c = b_ci[q];
+          float prod = a * b_val[q];                   /* line 6: value <- a_ij b_jk (float) */
+          if (mark[c] != i) {                          /* line 7: c_ik not in c_i*   */
+            mark[c] = i;
+            list.push_back(c);                         /* line 8: insert            */
+            acc[c] = prod;                             /* line 9: c_ik <- value     */
+            if (bound) absacc[c] = std::fabs((double)a) * std::fabs((double)b_val[q]);
+          } else {
+            acc[c] = acc[c] + prod;                    /* line 11: accumulate (float) */
+            if (bound) absacc[c] = absacc[c] + std::fabs((double)a) * std::fabs((double)b_val[q]);
           }
         }
       }

@@ -26,6 +26,7 @@ FLAG_VALIDATE = 1 << 0
 FLAG_INPUTS_REPLICATED = 1 << 1
 FLAG_PRECISE = 1 << 2
 FLAG_UPPER_BOUND = 1 << 3
+FLAG_FP32 = 1 << 4
 
 
 class SpgemmStats(ctypes.Structure):
@@ -105,6 +106,10 @@ def load():
     st = ctypes.c_int
     lib.spgemm_create.restype = st
     lib.spgemm_create.argtypes = [ctypes.POINTER(H), I64, I64, I64, P, P, P, I64, P, P, P, I64, P, ctypes.c_uint32]
+    lib.spgemm_create_f32.restype = st
+    lib.spgemm_create_f32.argtypes = [ctypes.POINTER(H), I64, I64, I64, P, P, P, I64, P, P, P, I64, P, ctypes.c_uint32]
+    lib.spgemm_numeric_f32.restype = st
+    lib.spgemm_numeric_f32.argtypes = [H, P, P, P]
     lib.spgemm_symbolic.restype = st
     lib.spgemm_symbolic.argtypes = [H, ctypes.POINTER(I64)]
     lib.spgemm_numeric.restype = st

@@ -214,6 +214,8 @@ void free_symbolic(spgemm_handle_t h) {
   h->numeric_recorded = false;
 }
 
+size_t vbytes(spgemm_handle_t h) { return (h->flags & SPGEMM_FLAG_FP32) ? sizeof(float) : sizeof(double); }
+
 spgemm_status_t sync(spgemm_handle_t h) {
   CK(h, cudaStreamSynchronize(h->stream));
   return SPGEMM_SUCCESS;
@@ -254,7 +256,7 @@ spgemm_status_t long_grow_arena(spgemm_handle_t h, const int32_t* list, int64_t 
   const int64_t total = h->pinned[0];
   const int64_t end = h->long_entries + total;
   CK(h, vmm_ensure(&h->arena_col, size_t(end) * sizeof(int32_t)));
-  CK(h, vmm_ensure(&h->arena_val, size_t(end) * sizeof(double)));
+  CK(h, vmm_ensure(&h->arena_val, size_t(end) * vbytes(h)));
   CK(h, launch_long_assign(h->lst, list, nlist, h->loff, h->long_entries, h->ltable, h->log2c0, h->stream));
   h->long_entries = end;
   return SPGEMM_SUCCESS;
@@ -300,6 +302,7 @@ spgemm_status_t run_long(spgemm_handle_t h) {
   for (;;) {
     CK(h, cudaMemsetAsync(h->lovf_cnt, 0, sizeof(int32_t), h->stream));
     Stage3Args a{};
+    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
     a.A = h->A;
     a.B = h->B;
     a.b_nnz = h->b_nnz;
@@ -336,6 +339,9 @@ spgemm_status_t run_long(spgemm_handle_t h) {
 }
 
 }  // namespace
+
+static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c_col_idx,
+                                          double* c_val);
 
 extern "C" {
 
@@ -393,7 +399,7 @@ spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int
     return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "negative size");
   if (m > INT32_MAX || k > INT32_MAX || n > INT32_MAX)
     return fail(nullptr, SPGEMM_ERROR_INDEX_OVERFLOW, "m, k or n exceeds INT32_MAX");
-  const uint32_t known = SPGEMM_FLAG_VALIDATE | SPGEMM_FLAG_INPUTS_REPLICATED | SPGEMM_FLAG_PRECISE |
+  const uint32_t known = SPGEMM_FLAG_VALIDATE | SPGEMM_FLAG_INPUTS_REPLICATED | SPGEMM_FLAG_PRECISE | SPGEMM_FLAG_FP32 |
                          SPGEMM_FLAG_UPPER_BOUND;
   if (flags & ~known) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "unknown flag bits 0x%x", flags & ~known);
   if (!a_row_ptr || !b_row_ptr) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL row_ptr");
@@ -528,13 +534,14 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   // precise: C~ holds only the window-bitmap rows' sorted column sets (STRUCT); sum_cap counts
   // only those rows (ctil_capacity, CAP_PRECISE)
   AL(h, &h->ctil_col, h->sum_cap > 0 ? h->sum_cap : 1);
-  if (hybrid) AL(h, &h->ctil_val, h->sum_cap);
+  if (hybrid) AL(h, &h->ctil_val, (h->sum_cap * vbytes(h) + 7) / 8);  // values of C~ (fp64 or fp32)
   tr("C~ allocation");
   cudaEventRecord(h->ev[1], h->stream);
   // stage 3: one launch per non-empty class ([P:264] "only issue kernels for non-empty bins")
   for (int t = T_G1; t < T_LONG; ++t) {
     if (h->tier_count[t] == 0) continue;
     Stage3Args a{};
+    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
     a.A = h->A;
     a.B = h->B;
     a.b_nnz = h->b_nnz;
@@ -576,6 +583,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   } else if (h->nlong > 0) {
     // precise: structure of long rows from a bitmap over the column window
     Stage3Args a{};
+    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
     a.A = h->A;
     a.B = h->B;
     a.b_nnz = h->b_nnz;
@@ -632,6 +640,15 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
 spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c_col_idx,
                                double* c_val) {
   if (!h) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL handle");
+  if (h->flags & SPGEMM_FLAG_FP32)
+    return fail(h, SPGEMM_ERROR_INVALID_VALUE, "fp32 handle: use spgemm_numeric_f32");
+  return spgemm_numeric_any(h, c_row_ptr, c_col_idx, c_val);
+}
+
+}  // extern "C"
+
+static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c_col_idx,
+                                          double* c_val) {
   if (!h->sym_ok) return fail(h, SPGEMM_ERROR_INVALID_STATE, "numeric before a successful symbolic");
   if (!c_row_ptr || (h->nnz_c > 0 && (!c_col_idx || !c_val)))
     return fail(h, SPGEMM_ERROR_INVALID_VALUE, "NULL output pointer");
@@ -642,6 +659,7 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
   if (h->m > 0 && h->nnz_c > 0) {
     const bool precise = (h->flags & SPGEMM_FLAG_PRECISE) != 0;
     CopyArgs ca{};
+    ca.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
     ca.m = h->m;
     ca.perm = h->ws.perm;
     ca.long_first = h->long_first;
@@ -662,6 +680,8 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
       for (int t = T_G1; t < T_LONG; ++t) {
         if (h->tier_count[t] == 0) continue;
         Stage3Args a{};
+        a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
+    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;
@@ -690,6 +710,8 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
       }
       if (h->nlong > 0) {
         Stage3Args a{};
+        a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
+    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;
@@ -718,6 +740,26 @@ spgemm_status_t spgemm_numeric(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c
   cudaEventRecord(h->ev[5], h->stream);
   h->numeric_recorded = true;
   return SPGEMM_SUCCESS;
+}
+
+extern "C" {
+
+spgemm_status_t spgemm_create_f32(spgemm_handle_t* handle, int64_t m, int64_t k, int64_t n,
+                                  const int64_t* a_row_ptr, const int32_t* a_col_idx, const float* a_val,
+                                  int64_t a_nnz, const int64_t* b_row_ptr, const int32_t* b_col_idx,
+                                  const float* b_val, int64_t b_nnz, spgemm_stream_t stream, uint32_t flags) {
+  if (flags & SPGEMM_FLAG_INPUTS_REPLICATED)
+    return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "INPUTS_REPLICATED is a dist_* flag");
+  return spgemm_create(handle, m, k, n, a_row_ptr, a_col_idx, reinterpret_cast<const double*>(a_val), a_nnz,
+                       b_row_ptr, b_col_idx, reinterpret_cast<const double*>(b_val), b_nnz, stream,
+                       flags | SPGEMM_FLAG_FP32);
+}
+
+spgemm_status_t spgemm_numeric_f32(spgemm_handle_t h, int64_t* c_row_ptr, int32_t* c_col_idx, float* c_val) {
+  if (!h) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "NULL handle");
+  if (sg_is_dist(h) || !(h->flags & SPGEMM_FLAG_FP32))
+    return fail(h, SPGEMM_ERROR_INVALID_VALUE, "spgemm_numeric_f32 on an fp64 handle");
+  return spgemm_numeric_any(h, c_row_ptr, c_col_idx, reinterpret_cast<double*>(c_val));
 }
 
 spgemm_status_t spgemm_destroy(spgemm_handle_t h) {

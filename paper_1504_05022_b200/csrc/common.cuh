@@ -167,6 +167,25 @@ struct CsrView {
 // accumulated into a dense, already ordered array (no insertion, no sort).
 enum Mode : int { MODE_COUNT = 0, MODE_FILL = 1, MODE_STRUCT = 2, MODE_DENSE = 3 };
 
+// Value arithmetic of Algorithm 1 lines 6, 9, 11: products rounded separately (no FMA), sums
+// in the order of the walk.  V = double (SpDGEMM, the default) or float (SpSGEMM,
+// SPGEMM_FLAG_FP32 / spgemm_create_f32: the paper's single-precision runs [P:403], [P:663]).
+template <typename V> struct Arith;
+template <> struct Arith<double> {
+  __device__ static __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+template <> struct Arith<float> {
+  __device__ static __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+// Value arrays travel as double* through the argument structs; kernels instantiated for V
+// reinterpret them (float arrays when the handle is FP32).
+template <typename V> __host__ __device__ __forceinline__ const V* vcast(const double* p) {
+  return reinterpret_cast<const V*>(p);
+}
+template <typename V> __host__ __device__ __forceinline__ V* vcast(double* p) { return reinterpret_cast<V*>(p); }
+
 struct LongState;
 
 struct Stage3Args {
@@ -203,6 +222,7 @@ struct Stage3Args {
   int log2c0;
   int32_t* ovf_list;
   int32_t* ovf_cnt;
+  int f32;                     // values are float (SpSGEMM)
 };
 // Long-row bitmap tile width in 32-column words (spgemm_set_debug_long_tile; 0 = default).
 extern int64_t g_long_tile_words;
@@ -326,6 +346,7 @@ struct CopyArgs {
   int log2c0;
   int32_t* c_col;
   double* c_val;
+  int f32;                     // values are float
 };
 cudaError_t launch_copy(const CopyArgs& a, cudaStream_t s);
 

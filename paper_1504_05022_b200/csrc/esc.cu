@@ -56,7 +56,7 @@ __device__ __forceinline__ int esc_block_excl_scan(int v, int* total, int* s_w) 
 
 constexpr int kEscRadixBits = 6;  // digit width of the block radix sort (4 passes for 23-bit windows)
 
-template <int NT, int IPT, bool VALS>
+template <int NT, int IPT, bool VALS, typename V>
 struct EscSmem {
   static constexpr int U = NT * IPT;
   // the sort carries the 16-bit product index p; values stay in place (pval) and are
@@ -65,26 +65,26 @@ struct EscSmem {
                                    kEscRadixBits>;
   struct Rows {
     unsigned key[U];
-    double val[VALS ? U : 1];
+    V val[VALS ? U : 1];
   };
   union {
     typename Sort::TempStorage sort;
     Rows rows;
   };
-  double pval[VALS ? U : 1];
+  V pval[VALS ? U : 1];
 };
 
-template <int NT, int IPT, int MODE, typename IT>
+template <int NT, int IPT, int MODE, typename IT, typename V>
 __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
   constexpr bool VALS = MODE == MODE_FILL;
   constexpr int U = NT * IPT;
   constexpr int NW = NT / 32;
-  using SM = EscSmem<NT, IPT, VALS>;
+  using SM = EscSmem<NT, IPT, VALS, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   __shared__ IT s_bs[NT];
   __shared__ int s_len[NT], s_pex[NT];
-  __shared__ double s_av[VALS ? NT : 1];
+  __shared__ V s_av[VALS ? NT : 1];
   __shared__ int s_w[NW + 1];
   __shared__ unsigned s_max[NW];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
         const int64_t b0 = __ldg(a.B.rp + j);
         len = (int)(__ldg(a.B.rp + j + 1) - b0);
         s_bs[tid] = (IT)b0;
-        if (VALS) s_av[tid] = __ldg(a.A.val + e);
+        if (VALS) s_av[tid] = __ldg(vcast<V>(a.A.val) + e);
       }
       int tot;
       const int ex = esc_block_excl_scan<NT>(len, &tot, s_w);  // syncs
@@ -117,12 +117,12 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
       for (int t = w; t < na; t += NW) {
         const IT bs = s_bs[t];
         const int lt = s_len[t], pe = s_pex[t];
-        const double at = VALS ? s_av[t] : 0.0;
+        const V at = VALS ? s_av[t] : V(0);
         for (int q = lane; q < lt; q += 32) {
           const unsigned k = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
           sm.rows.key[pe + q] = k;
           kmax = k > kmax ? k : kmax;
-          if (VALS) sm.pval[pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
+          if (VALS) sm.pval[pe + q] = Arith<V>::mul(at, __ldg(vcast<V>(a.B.val) + bs + q));  // line 6
         }
       }
       u += tot;
@@ -157,12 +157,12 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
     __syncthreads();
     const unsigned pad = end_bit >= 32 ? 0xffffffffu : ((1u << end_bit) - 1u);
     (void)pad;
-    double v[IPT];
+    V v[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       sm.rows.key[tid * IPT + i] = k[i];
       if constexpr (VALS) {
-        v[i] = tid * IPT + i < u ? sm.pval[pi[i]] : 0.0;
+        v[i] = tid * IPT + i < u ? sm.pval[pi[i]] : V(0);
         sm.rows.val[tid * IPT + i] = v[i];
       }
     }
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
       if (head) {
         ++heads;
         if constexpr (VALS) {
-          double acc = v[i];
-          for (int x = p + 1; x < u && sm.rows.key[x] == k[i]; ++x) acc = __dadd_rn(acc, sm.rows.val[x]);
+          V acc = v[i];
+          for (int x = p + 1; x < u && sm.rows.key[x] == k[i]; ++x) acc = Arith<V>::add(acc, sm.rows.val[x]);
           v[i] = acc;
         }
       } else {
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
       const int64_t o = __ldg(a.out_off + row);
       for (int i = tid; i < nnz; i += NT) {
         a.out_col[o + i] = (int)sm.rows.key[i] + lo;
-        if constexpr (VALS) a.out_val[o + i] = sm.rows.val[i];
+        if constexpr (VALS) vcast<V>(a.out_val)[o + i] = sm.rows.val[i];
       }
     }
     if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
@@ -207,11 +207,11 @@ __global__ void __launch_bounds__(NT) k_esc_sort(Stage3Args a) {
   }
 }
 
-template <int NT, int IPT, int MODE, typename IT>
+template <int NT, int IPT, int MODE, typename IT, typename V>
 cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
-  using SM = EscSmem<NT, IPT, MODE == MODE_FILL>;
+  using SM = EscSmem<NT, IPT, MODE == MODE_FILL, V>;
   const size_t bytes = sizeof(SM);
-  auto kern = k_esc_sort<NT, IPT, MODE, IT>;
+  auto kern = k_esc_sort<NT, IPT, MODE, IT, V>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -231,25 +231,25 @@ cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
 // rounds instead of one radix pass per digit.  Each round: thread t produces output positions
 // [t·IPT, (t+1)·IPT): binary search for its pair of runs and its merge-path split, then a
 // sequential merge; keys and values ping-pong between two shared buffers.
-template <int NT, int IPT>
+template <int NT, int IPT, typename V>
 struct MergeSmem {
   static constexpr int U = NT * IPT;
   unsigned key[2][U];
   unsigned short idx[2][U];  // product position p: values stay in pval until the compression
-  double pval[U];
+  V pval[U];
   unsigned short rb[U + 2];  // run boundaries (nonempty runs)
 };
 
-template <int NT, int IPT, typename IT>
+template <int NT, int IPT, typename IT, typename V>
 __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
   constexpr int U = NT * IPT;
   constexpr int NW = NT / 32;
-  using SM = MergeSmem<NT, IPT>;
+  using SM = MergeSmem<NT, IPT, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   __shared__ IT s_bs[NT];
   __shared__ int s_len[NT], s_pex[NT];
-  __shared__ double s_av[NT];
+  __shared__ V s_av[NT];
   __shared__ int s_w[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
         const int64_t b0 = __ldg(a.B.rp + j);
         len = (int)(__ldg(a.B.rp + j + 1) - b0);
         s_bs[tid] = (IT)b0;
-        s_av[tid] = __ldg(a.A.val + e);
+        s_av[tid] = __ldg(vcast<V>(a.A.val) + e);
       }
       int tot, rtot;
       const int ex = esc_block_excl_scan<NT>(len, &tot, s_w);
@@ -282,11 +282,11 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
       for (int t = w; t < na; t += NW) {
         const IT bs = s_bs[t];
         const int lt = s_len[t], pe = s_pex[t];
-        const double at = s_av[t];
+        const V at = s_av[t];
         for (int q = lane; q < lt; q += 32) {
           sm.key[0][pe + q] = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
           sm.idx[0][pe + q] = (unsigned short)(pe + q);
-          sm.pval[pe + q] = __dmul_rn(at, __ldg(a.B.val + bs + q));  // line 6
+          sm.pval[pe + q] = Arith<V>::mul(at, __ldg(vcast<V>(a.B.val) + bs + q));  // line 6
         }
       }
       u += tot;
@@ -366,12 +366,12 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
     int nnz;
     int pos = esc_block_excl_scan<NT>(heads, &nnz, s_w);
     const int64_t o = __ldg(a.out_off + row);
-    double vh[IPT];
+    V vh[IPT];
     for (int i = 0; i < IPT; ++i) {
       const int p = tid * IPT + i;
       if (p < u && (p == 0 || key[p - 1] != key[p])) {
-        double acc = sm.pval[idx[p]];
-        for (int x = p + 1; x < u && key[x] == key[p]; ++x) acc = __dadd_rn(acc, sm.pval[idx[x]]);
+        V acc = sm.pval[idx[p]];
+        for (int x = p + 1; x < u && key[x] == key[p]; ++x) acc = Arith<V>::add(acc, sm.pval[idx[x]]);
         vh[i] = acc;
       }
     }
@@ -387,17 +387,17 @@ __global__ void __launch_bounds__(NT) k_esc_merge(Stage3Args a) {
     __syncthreads();
     for (int i = tid; i < nnz; i += NT) {
       a.out_col[o + i] = (int)sm.key[b ^ 1][i] + lo;
-      a.out_val[o + i] = sm.pval[i];
+      vcast<V>(a.out_val)[o + i] = sm.pval[i];
     }
     if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncthreads();
   }
 }
 
-template <int NT, int IPT, typename IT>
+template <int NT, int IPT, typename IT, typename V>
 cudaError_t launch_merge_k(const Stage3Args& a, cudaStream_t s) {
-  const size_t bytes = sizeof(MergeSmem<NT, IPT>);
-  auto kern = k_esc_merge<NT, IPT, IT>;
+  const size_t bytes = sizeof(MergeSmem<NT, IPT, V>);
+  auto kern = k_esc_merge<NT, IPT, IT, V>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -413,7 +413,9 @@ cudaError_t launch_merge_k(const Stage3Args& a, cudaStream_t s) {
 template <int NT, int IPT>
 cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
-  return i32 ? launch_esc_k<NT, IPT, MODE_FILL, int>(a, s) : launch_esc_k<NT, IPT, MODE_FILL, int64_t>(a, s);
+  if (a.f32)
+    return i32 ? launch_esc_k<NT, IPT, MODE_FILL, int, float>(a, s) : launch_esc_k<NT, IPT, MODE_FILL, int64_t, float>(a, s);
+  return i32 ? launch_esc_k<NT, IPT, MODE_FILL, int, double>(a, s) : launch_esc_k<NT, IPT, MODE_FILL, int64_t, double>(a, s);
 }
 
 // Merge kernels use an odd number of items per thread: each thread reads and writes its own
@@ -421,7 +423,8 @@ cudaError_t launch_esc_t(const Stage3Args& a, cudaStream_t s) {
 template <int NT, int IPT>
 cudaError_t launch_merge_t(const Stage3Args& a, cudaStream_t s) {
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
-  return i32 ? launch_merge_k<NT, IPT, int>(a, s) : launch_merge_k<NT, IPT, int64_t>(a, s);
+  if (a.f32) return i32 ? launch_merge_k<NT, IPT, int, float>(a, s) : launch_merge_k<NT, IPT, int64_t, float>(a, s);
+  return i32 ? launch_merge_k<NT, IPT, int, double>(a, s) : launch_merge_k<NT, IPT, int64_t, double>(a, s);
 }
 
 }  // namespace

@@ -254,13 +254,13 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax)
 // entries do not fit the row's current capacity is the checkpoint — the row stops there
 // (earlier tiles stay written), reports how much it needs, and resumes at that tile after the
 // host has grown its allocation.
-template <int NT, bool PROG>
+template <int NT, bool PROG, typename VT>
 __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
   int* pre = reinterpret_cast<int*>(smem + size_t(tmax) * sizeof(unsigned));
-  double* vals = reinterpret_cast<double*>(smem + size_t(tmax) * 8);  // V values of a rank window
+  VT* vals = reinterpret_cast<VT*>(smem + size_t(tmax) * 8);  // V values of a rank window
   __shared__ int s_red[2 * NW];
   __shared__ int s_w[NW + 1];
   __shared__ Batch<NT> sb;
@@ -274,12 +274,12 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
     const int row = __ldg(a.perm + a.first + (PROG ? int64_t(k_long) : r));
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int32_t* oc;
-    double* ov;
+    VT* ov;
     int64_t done = 0;  // entries of the row placed by earlier tiles
     int64_t cap = 0, start = INT64_MIN;
     if (PROG) {
       oc = a.arena_col;
-      ov = a.arena_val;
+      ov = vcast<VT>(a.arena_val);
       const LongState st = a.lst[k_long];
       done = st.count;
       cap = st.cap;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
     } else {
       const int64_t o = __ldg(a.out_off + row);
       oc = a.out_col + o;
-      ov = a.out_val + o;
+      ov = vcast<VT>(a.out_val) + o;
     }
     // row position p -> element of oc / ov
     auto at_pos = [&](int64_t p) -> int64_t { return PROG ? s_tab[chunk_of(p, a.log2c0)] + p : p; };
@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
           }
         }
         for (int i = threadIdx.x; i < wn; i += NT) {  // the identity of + (line 9's assignment)
-          if (insm) vals[i] = -0.0;
-          else ov[at_pos(done + i)] = -0.0;
+          if (insm) vals[i] = VT(-0.0);
+          else ov[at_pos(done + i)] = VT(-0.0);
         }
         __syncthreads();
         for (int64_t e0 = a0; e0 < a1; e0 += NT) {
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
             const int4 bw = __ldg(a.bwin + j);
             const int64_t bs = __ldg(a.B.rp + j);
             sb.bs[threadIdx.x] = bs;
-            sb.av[threadIdx.x] = __ldg(a.A.val + e);
+            sb.av[threadIdx.x] = (double)__ldg(vcast<VT>(a.A.val) + e);  // exact for float too
             // lower bounds of the warps' column boundaries in b_j* (binary searches advanced
             // in lockstep, their loads in flight together): first the window's own segment
             // [s0, s1) (pruned by b_j*'s first / last column), then the NW-1 interior
@@ -437,13 +437,13 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
             const int s0 = s_split[t][w], en = s_split[t][w + 1];
             if (s0 >= en) continue;
             const int32_t* __restrict__ sc = a.B.ci + sb.bs[t];
-            const double* __restrict__ sv = a.B.val + sb.bs[t];
-            const double at = sb.av[t];
+            const VT* __restrict__ sv = vcast<VT>(a.B.val) + sb.bs[t];
+            const VT at = (VT)sb.av[t];
             // columns inside one b_j* are distinct: the chunks of a segment touch distinct
             // outputs, so four of them are gathered, ranked and updated together
             for (int q0 = s0; q0 < en; q0 += 128) {
               int x[4];
-              double v[4], old[4];
+              VT v[4], old[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int q = q0 + 32 * u + lane;
@@ -461,9 +461,9 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
                   if (x[u] >= 0) old[u] = vals[x[u]];
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) vals[x[u]] = __dadd_rn(old[u], __dmul_rn(at, v[u]));  // lines 6, 9, 11
+                  if (x[u] >= 0) vals[x[u]] = Arith<VT>::add(old[u], Arith<VT>::mul(at, v[u]));  // lines 6, 9, 11
               } else {
-                double* p[4];
+                VT* p[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                   if (x[u] >= 0) {
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
                   }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) *p[u] = __dadd_rn(old[u], __dmul_rn(at, v[u]));
+                  if (x[u] >= 0) *p[u] = Arith<VT>::add(old[u], Arith<VT>::mul(at, v[u]));
               }
             }
             __syncwarp();  // the next segment may add into a column this one just wrote
@@ -595,7 +595,8 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   int per_sm = 1;
   cudaError_t e;
   if (fill) {
-    auto kern = a.lst ? k_long_rank<kRkNT, true> : k_long_rank<kRkNT, false>;
+    auto kern = a.f32 ? (a.lst ? k_long_rank<kRkNT, true, float> : k_long_rank<kRkNT, false, float>)
+                      : (a.lst ? k_long_rank<kRkNT, true, double> : k_long_rank<kRkNT, false, double>);
     // two CTAs per SM: the rest of a CTA's share of shared memory holds the values of a rank
     // window (c3b: 64 KB of bits and ranks, 4 Ki values)
     cudaFuncAttributes fa;

@@ -31,11 +31,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // --------------------------------------------------------------- G-lane sort groups
-template <int G, int NT, bool KEY32>
+template <int G, int NT, bool KEY32, typename V>
 __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two <= 32");
   __shared__ int s_col[NT];
-  __shared__ double s_val[NT];
+  __shared__ V s_val[NT];
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int gfirst = threadIdx.x & ~(G - 1);
@@ -64,15 +64,15 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
     }
     int cnt = 0;  // products gathered so far in this group
     unsigned long long key = ~0ull;
-    double myv = 0.0;
+    V myv = V(0);
     for (int64_t e0 = 0; e0 < maxlen; e0 += G) {
       const int64_t e = a0 + e0 + gl;
       int len = 0;
       int64_t bs = 0;
-      double av = 0.0;
+      V av = V(0);
       if (e < a1) {
         const int j = __ldg(a.A.ci + e);
-        if (fill) av = __ldg(a.A.val + e);
+        if (fill) av = __ldg(vcast<V>(a.A.val) + e);
         bs = __ldg(a.B.rp + j);
         len = (int)(__ldg(a.B.rp + j + 1) - bs);
       }
@@ -91,13 +91,13 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
         if (v <= q) lo += step;
       }
       const int64_t obs = __shfl_sync(0xffffffffu, bs, lo, G);
-      const double oa = __shfl_sync(0xffffffffu, av, lo, G);
+      const V oa = __shfl_sync(0xffffffffu, av, lo, G);
       const int oex = __shfl_sync(0xffffffffu, inc - len, lo, G);
       if (q >= 0 && q < tot) {
         const int64_t qq = obs + (q - oex);
         const int c = __ldg(a.B.ci + qq);
         key = ((unsigned long long)(unsigned)c << 32) | (unsigned)gl;
-        if (fill) myv = __dmul_rn(oa, __ldg(a.B.val + qq));   // line 6: value <- a_ij b_jk
+        if (fill) myv = Arith<V>::mul(oa, __ldg(vcast<V>(a.B.val) + qq));  // line 6: value <- a_ij b_jk
       }
       cnt += tot;
     }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
       col = valid ? (int)(key >> 32) : -1;
       src = (int)(key & 31u);
     }
-    const double v = __shfl_sync(0xffffffffu, myv, valid ? src : gl, G);
+    const V v = __shfl_sync(0xffffffffu, myv, valid ? src : gl, G);
     const int prev = __shfl_up_sync(0xffffffffu, col, 1, G);
     const bool head = valid && (gl == 0 || prev != col);
     const unsigned hb = __ballot_sync(0xffffffffu, head) & gbits;
@@ -153,13 +153,13 @@ __global__ void __launch_bounds__(NT) k_group(Stage3Args a) {
       s_val[threadIdx.x] = v;
       __syncwarp();
       if (has && head) {
-        double acc = v;                                    // line 9: c_ik <- value
+        V acc = v;                                          // line 9: c_ik <- value
         for (int t = gl + 1; t < G && s_col[gfirst + t] == col; ++t)
-          acc = __dadd_rn(acc, s_val[gfirst + t]);         // line 11: c_ik += value
+          acc = Arith<V>::add(acc, s_val[gfirst + t]);      // line 11: c_ik += value
         const int pos = __popc(hb & lanemask_lt());
         const int64_t o = __ldg(a.out_off + row) + pos;
         a.out_col[o] = col;
-        a.out_val[o] = acc;
+        vcast<V>(a.out_val)[o] = acc;
       }
       __syncwarp();
     }
@@ -262,9 +262,12 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   constexpr size_t per_slot = 4;  // k_cta_hash counts only
   switch (tier) {
-#define SG_GROUP(G, UPB)                                                                      \
-  return a.n < (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true>, 256, 0, a.count, UPB, a, s) \
-                                   : launch_persistent(k_group<G, 256, false>, 256, 0, a.count, UPB, a, s)
+#define SG_GROUP(G, UPB)                                                                              \
+  if (a.f32 && a.mode == MODE_FILL)                                                                     \
+    return a.n < (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true, float>, 256, 0, a.count, UPB, a, s) \
+                                     : launch_persistent(k_group<G, 256, false, float>, 256, 0, a.count, UPB, a, s); \
+  return a.n < (int64_t(1) << 27) ? launch_persistent(k_group<G, 256, true, double>, 256, 0, a.count, UPB, a, s) \
+                                   : launch_persistent(k_group<G, 256, false, double>, 256, 0, a.count, UPB, a, s)
     case T_G1: SG_GROUP(1, 256);
     case T_G2: SG_GROUP(2, 128);
     case T_G4: SG_GROUP(4, 64);

@@ -12,6 +12,7 @@ namespace {
 // Flat copy: warp w owns rows [32w, 32w+32); their outputs form one contiguous span of C.
 // Lane p-th output finds its row by a shuffle binary search over the 33 row pointers, so
 // every store instruction writes 32 consecutive entries.
+template <typename V>
 __global__ void __launch_bounds__(256) k_copy_flat(CopyArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (a.m + 31) / 32;
@@ -40,13 +41,14 @@ __global__ void __launch_bounds__(256) k_copy_flat(CopyArgs a) {
       if (p < end && !rl) {
         const int64_t q = rsrc + (p - rbeg);
         a.c_col[p] = __ldcs(a.ctil_col + q);
-        a.c_val[p] = __ldcs(a.ctil_val + q);
+        vcast<V>(a.c_val)[p] = __ldcs(vcast<V>(a.ctil_val) + q);
       }
     }
   }
 }
 
 // long rows: their C~ slice lives in the long-row arena behind the row's chunk table
+template <typename V>
 __global__ void __launch_bounds__(512) k_copy_long(CopyArgs a) {
   const int64_t k = blockIdx.x;
   const int row = a.perm[a.long_first + k];
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(512) k_copy_long(CopyArgs a) {
   for (int64_t t = threadIdx.x; t < len; t += blockDim.x) {
     const int64_t x = __ldg(tab + chunk_of(t, a.log2c0)) + t;
     a.c_col[d + t] = __ldcs(a.arena_col + x);
-    a.c_val[d + t] = __ldcs(a.arena_val + x);
+    vcast<V>(a.c_val)[d + t] = __ldcs(vcast<V>(a.arena_val) + x);
   }
 }
 
@@ -73,12 +75,14 @@ cudaError_t launch_copy(const CopyArgs& a, cudaStream_t s) {
   if (a.m > 0) {
     const int64_t cap = int64_t(sms()) * 16;
     const int64_t g2 = ((a.m + 31) / 32 + 7) / 8;
-    k_copy_flat<<<(unsigned)(g2 < cap ? g2 : cap), 256, 0, s>>>(a);
+    if (a.f32) k_copy_flat<float><<<(unsigned)(g2 < cap ? g2 : cap), 256, 0, s>>>(a);
+    else k_copy_flat<double><<<(unsigned)(g2 < cap ? g2 : cap), 256, 0, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (a.nlong > 0) {
-    k_copy_long<<<(unsigned)a.nlong, 512, 0, s>>>(a);
+    if (a.f32) k_copy_long<float><<<(unsigned)a.nlong, 512, 0, s>>>(a);
+    else k_copy_long<double><<<(unsigned)a.nlong, 512, 0, s>>>(a);
     return cudaGetLastError();
   }
   return cudaSuccess;

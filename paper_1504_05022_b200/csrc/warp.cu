@@ -77,19 +77,19 @@ __device__ __forceinline__ unsigned winsert(int* keys, int* list, int& cnt, int 
 // One a_ij chunk (up to 32 entries of row i of A): lane e holds b_j*'s start and length and a_ij.
 // IT: index type of B's entries (int32_t when nnz(B) < 2^31: one shuffle and one IMAD.WIDE per
 // address instead of 64-bit arithmetic).
-template <typename IT>
+template <typename IT, typename V>
 struct AChunk {
   IT bs;
   int len;
-  double av;
+  V av;
 };
 
-template <bool VALS, typename IT>
-__device__ __forceinline__ AChunk<IT> load_achunk(const Stage3Args& a, int64_t e, int64_t a1) {
-  AChunk<IT> ch{0, 0, 0.0};
+template <bool VALS, typename IT, typename V>
+__device__ __forceinline__ AChunk<IT, V> load_achunk(const Stage3Args& a, int64_t e, int64_t a1) {
+  AChunk<IT, V> ch{0, 0, V(0)};
   if (e < a1) {
     const int j = __ldg(a.A.ci + e);
-    if (VALS) ch.av = __ldg(a.A.val + e);
+    if (VALS) ch.av = __ldg(vcast<V>(a.A.val) + e);
     const int64_t b0 = __ldg(a.B.rp + j);
     ch.bs = (IT)b0;
     ch.len = (int)(__ldg(a.B.rp + j + 1) - b0);
@@ -100,24 +100,17 @@ __device__ __forceinline__ AChunk<IT> load_achunk(const Stage3Args& a, int64_t e
 constexpr int kGroup = 4;  // b_j* whose loads are in flight together
 
 // Walk all products of row i in Algorithm-1 order, calling op(c, v, at, act) once per b_j*
-// segment of up to 32 entries (c: this lane's column, v: b_jk, at: a_ij).
-// avs (VALS only, optional): a 32-double shared buffer of the warp; a_ij is then broadcast from
-// it (one LDS.64) instead of two shuffles per b_j*.
-template <bool VALS, typename IT, typename Op>
-__device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_t a1, int lane, Op&& op,
-                                         unsigned avs = 0u) {
+// segment of up to 32 entries (c: this lane's column, v: b_jk, at: a_ij; V the value type).
+template <bool VALS, typename IT, typename V, typename Op>
+__device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_t a1, int lane, Op&& op) {
+  const V* __restrict__ bval = vcast<V>(a.B.val);
   for (int64_t e0 = a0; e0 < a1; e0 += 32) {
-    const AChunk<IT> ch = load_achunk<VALS, IT>(a, e0 + lane, a1);
+    const AChunk<IT, V> ch = load_achunk<VALS, IT, V>(a, e0 + lane, a1);
     const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
-    if (VALS && avs) {
-      __syncwarp();
-      asm volatile("st.shared.f64 [%0], %1;" ::"r"(avs + 8u * lane), "d"(ch.av) : "memory");
-      __syncwarp();
-    }
     if (!__any_sync(kFull, ch.len > 32)) {
       for (int t0 = 0; t0 < nE; t0 += kGroup) {
         int c[kGroup];
-        double v[kGroup], at[kGroup];
+        V v[kGroup], at[kGroup];
         bool act[kGroup];
 #pragma unroll
         for (int u = 0; u < kGroup; ++u) {
@@ -127,28 +120,24 @@ __device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_
           act[u] = lane < len;
           c[u] = act[u] ? __ldg(a.B.ci + q) : kEmptyKey;
           if (VALS) {
-            if (avs) {
-              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(at[u]) : "r"(avs + 8u * t) : "memory");
-            } else {
-              at[u] = __shfl_sync(kFull, ch.av, t);
-            }
-            v[u] = act[u] ? __ldg(a.B.val + q) : 0.0;
+            at[u] = __shfl_sync(kFull, ch.av, t);
+            v[u] = act[u] ? __ldg(bval + q) : V(0);
           }
         }
 #pragma unroll
         for (int u = 0; u < kGroup; ++u)
-          if (t0 + u < nE) op(c[u], VALS ? v[u] : 0.0, VALS ? at[u] : 0.0, act[u]);
+          if (t0 + u < nE) op(c[u], VALS ? v[u] : V(0), VALS ? at[u] : V(0), act[u]);
       }
     } else {
       for (int t = 0; t < nE; ++t) {
         const IT bs = __shfl_sync(kFull, ch.bs, t);
         const int len = __shfl_sync(kFull, ch.len, t);
-        const double at = VALS ? __shfl_sync(kFull, ch.av, t) : 0.0;
+        const V at = VALS ? __shfl_sync(kFull, ch.av, t) : V(0);
         for (int q0 = 0; q0 < len; q0 += 32) {
           const bool act = q0 + lane < len;
           const IT q = bs + (IT)(q0 + lane);
           const int c = act ? __ldg(a.B.ci + q) : kEmptyKey;
-          const double v = (VALS && act) ? __ldg(a.B.val + q) : 0.0;
+          const V v = (VALS && act) ? __ldg(bval + q) : V(0);
           op(c, v, at, act);
         }
       }
@@ -162,15 +151,22 @@ __device__ __forceinline__ void walk_row(const Stage3Args& a, int64_t a0, int64_
 // two or three shuffles per b_j* — and the steps of four b_j* are issued back to back (their
 // gathers in flight together).  Records of lanes past the row's end have nnz 0, so the
 // four-step groups need no bounds check: those steps run with every lane idle (act false).
-template <bool VALS, typename Op>
-__device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci, const double* __restrict__ aval,
+template <typename V>
+__device__ __forceinline__ V rec_val(const int4& r);
+template <>
+__device__ __forceinline__ double rec_val<double>(const int4& r) { return __hiloint2double(r.w, r.z); }
+template <>
+__device__ __forceinline__ float rec_val<float>(const int4& r) { return __int_as_float(r.z); }
+
+template <bool VALS, typename V, typename Op>
+__device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci, const V* __restrict__ aval,
                                                 const int64_t* __restrict__ brp, const int32_t* __restrict__ bci,
-                                                const double* __restrict__ bval, int64_t a0, int64_t a1,
+                                                const V* __restrict__ bval, int64_t a0, int64_t a1,
                                                 int lane, unsigned stage, Op&& op) {
   for (int64_t e0 = a0; e0 < a1; e0 += 32) {
     const int64_t e = e0 + lane;
     int bs = 0, len = 0;
-    double av = 0.0;
+    V av = V(0);
     if (e < a1) {
       const int j = __ldg(aci + e);
       const int64_t b0 = __ldg(brp + j);
@@ -178,15 +174,18 @@ __device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci,
       len = (int)(__ldg(brp + j + 1) - b0);
       if (VALS) av = __ldg(aval + e);
     }
+    const double avd = (double)av;  // record bits: the double, or the float in the low word
+    const int lo_w = sizeof(V) == 8 ? __double2loint(avd) : __float_as_int((float)av);
+    const int hi_w = sizeof(V) == 8 ? __double2hiint(avd) : 0;
     __syncwarp();
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stage + 16u * lane), "r"(bs), "r"(len),
-                 "r"(__double2loint(av)), "r"(__double2hiint(av)) : "memory");
+                 "r"(lo_w), "r"(hi_w) : "memory");
     __syncwarp();
     const int nE = (int)((a1 - e0) < 32 ? (a1 - e0) : 32);
     if (!__any_sync(kFull, len > 32)) {
       for (int t0 = 0; t0 < nE; t0 += kGroup) {
         int c[kGroup];
-        double v[kGroup], at[kGroup];
+        V v[kGroup], at[kGroup];
         bool act[kGroup];
 #pragma unroll
         for (int u = 0; u < kGroup; ++u) {
@@ -197,8 +196,8 @@ __device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci,
           const int q = r.x + lane;
           c[u] = act[u] ? __ldg(bci + q) : kEmptyKey;
           if (VALS) {
-            at[u] = __hiloint2double(r.w, r.z);
-            v[u] = act[u] ? __ldg(bval + q) : 0.0;
+            at[u] = rec_val<V>(r);
+            v[u] = act[u] ? __ldg(bval + q) : V(0);
           }
         }
 #pragma unroll
@@ -223,13 +222,13 @@ __device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci,
 }
 
 // walk_row_staged when B's offsets fit 32 bits and the kernel has a stage buffer, else walk_row.
-template <bool VALS, typename IT, typename Op>
+template <bool VALS, typename IT, typename V, typename Op>
 __device__ __forceinline__ void walk_any(const Stage3Args& a, int64_t a0, int64_t a1, int lane, unsigned stage,
                                          Op&& op) {
   if constexpr (std::is_same<IT, int>::value) {
-    walk_row_staged<VALS>(a.A.ci, a.A.val, a.B.rp, a.B.ci, a.B.val, a0, a1, lane, stage, op);
+    walk_row_staged<VALS, V>(a.A.ci, vcast<V>(a.A.val), a.B.rp, a.B.ci, vcast<V>(a.B.val), a0, a1, lane, stage, op);
   } else {
-    walk_row<VALS, IT>(a, a0, a1, lane, op);
+    walk_row<VALS, IT, V>(a, a0, a1, lane, op);
   }
 }
 
@@ -252,7 +251,7 @@ __global__ void __launch_bounds__(NW * 32) k_wrow(Stage3Args a) {
     for (int s = lane; s < S / 4; s += 32) k4[s] = make_int4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
     __syncwarp();
     int cnt = 0;
-    walk_row<false, IT>(a, a0, a1, lane, [=, &cnt](int c, double, double, bool act) {
+    walk_row<false, IT, double>(a, a0, a1, lane, [=, &cnt](int c, double, double, bool act) {
       winsert<LOG2S, false>(keys, nullptr, cnt, c, act);  // lines 7-8 / 10
     });
     __syncwarp();
@@ -321,6 +320,20 @@ __device__ __forceinline__ double sh_ld_f64(unsigned addr) {
 }
 __device__ __forceinline__ void sh_st_f64(unsigned addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v));
+}
+template <typename V>
+__device__ __forceinline__ V sh_ldv(unsigned addr);
+template <>
+__device__ __forceinline__ double sh_ldv<double>(unsigned addr) { return sh_ld_f64(addr); }
+template <>
+__device__ __forceinline__ float sh_ldv<float>(unsigned addr) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void sh_stv(unsigned addr, double v) { sh_st_f64(addr, v); }
+__device__ __forceinline__ void sh_stv(unsigned addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
 }
 __device__ __forceinline__ int4 sh_ld_v4(unsigned addr) {
   int4 r;
@@ -392,7 +405,7 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
   return L;
 }
 
-template <int MODE, typename IT>
+template <int MODE, typename IT, typename V>
 __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   constexpr bool SUMM = MODE == MODE_STRUCT || MODE == MODE_FILL;  // products -> bits + summary
   extern __shared__ __align__(16) uint32_t s_bw[];
@@ -427,7 +440,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       // summary: only the lane that finds a word empty sets its summary bit, so summary
       // atomics are rare and seldom share an address.
       // Branch-free: an idle lane (act false) re-sets the bit of column lo, a column of the row.
-      walk_row<false, IT>(a, a0, a1, lane, [=](int c, double, double, bool act) {
+      walk_row<false, IT, V>(a, a0, a1, lane, [=](int c, V, V, bool act) {
         const unsigned d = act ? (unsigned)(c - lo) : 0u;
         const unsigned wa = bm + ((d >> 5) << 2);
         if (SUMM) {
@@ -543,8 +556,8 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         // so each word takes one RED (same-address REDs serialise: 7.6x the ideal wavefronts)
         const int wkey = in ? (d >> 5) : -1 - lane;
         unsigned wbits = in ? 1u << (d & 31) : 0u;
-#pragma unroll
-        for (int sh = 1; sh < 32; sh <<= 1) {
+#pragma unroll 1
+        for (int sh = 1; sh < 32; sh <<= 1) {  // (not unrolled: keeps the kernel at 48 registers)
           const unsigned vo = __shfl_down_sync(kFull, wbits, sh);
           const int ko = __shfl_down_sync(kFull, wkey, sh);
           if (lane + sh < 32 && ko == wkey) wbits |= vo;
@@ -562,14 +575,14 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
         prevd = __shfl_sync(kFull, d, 31);
       }
     }
-    for (int p = lane; p < nnz; p += 32) sh_st_f64(vals + 8u * p, -0.0);  // identity of +: first add == line 9
+    for (int p = lane; p < nnz; p += 32) sh_stv(vals + 8u * p, V(-0.0));  // identity of +: first add == line 9
     __syncwarp();
     // lines 6, 9, 11: c_ik += a_ij b_jk at the column's rank
     // Branch-free: an idle lane looks up column lo (present) and adds into a scratch slot.
     // Lanes of one b_j* hold distinct columns, so no two lanes of an instruction share a slot;
     // successive b_j* are ordered by the warp's in-order shared-memory accesses.
     const unsigned scratch = vals + 8u * unsigned(L.nv);
-    auto accumulate = [=](int c, double v, double at, bool act) {
+    auto accumulate = [=](int c, V v, V at, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       unsigned word, base;
       if (MODE == MODE_DENSE) {  // one 8-byte record: the word's bits and its first rank
@@ -584,13 +597,13 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       }
       const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
-      sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
+      sh_stv(va, Arith<V>::add(sh_ldv<V>(va), Arith<V>::mul(at, v)));
     };
-    if (MODE == MODE_DENSE) walk_any<true, IT>(a, a0, a1, lane, bm + L.o_stage, accumulate);
-    else walk_row<true, IT>(a, a0, a1, lane, accumulate);
+    if (MODE == MODE_DENSE) walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
+    else walk_row<true, IT, V>(a, a0, a1, lane, accumulate);
     __syncwarp();
-    double* ov = a.out_val + o;
-    for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
+    V* ov = vcast<V>(a.out_val) + o;
+    for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
     if (MODE == MODE_FILL) {
       for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
     } else {
@@ -634,7 +647,7 @@ __host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns, bool fill,
   return L;
 }
 
-template <typename IT, bool FILL>
+template <typename IT, bool FILL, typename V>
 __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -654,7 +667,7 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
     int nslot = 0;  // warp-uniform
-    walk_any<false, IT>(a, a0, a1, lane, stage, [=, &nslot](int c, double, double, bool act) {
+    walk_any<false, IT, V>(a, a0, a1, lane, stage, [=, &nslot](int c, V, V, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
       const unsigned blk = d >> 10;
       unsigned s = act ? sh_ld_u16(dir + 2u * blk) : 1u;
@@ -712,20 +725,20 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     }
     if (FILL) {
       // lines 6, 9, 11: values at the columns' ranks (as the DENSE numeric kernel), then clear
-      for (int p = lane; p < nnz; p += 32) sh_st_f64(vals + 8u * p, -0.0);
+      for (int p = lane; p < nnz; p += 32) sh_stv(vals + 8u * p, V(-0.0));
       __syncwarp();
       const unsigned scratch = vals + 8u * unsigned(L.nv);
-      walk_row<true, IT>(a, a0, a1, lane, [=](int c, double v, double at, bool act) {
+      walk_row<true, IT, V>(a, a0, a1, lane, [=](int c, V v, V at, bool act) {
         const unsigned d = act ? (unsigned)(c - lo) : 0u;
         const unsigned wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
         const unsigned word = sh_ld(bits + 4u * wi);
         const unsigned rank = sh_ld_u16(pre + 2u * wi) + __popc(word & ((1u << (d & 31)) - 1u));
         const unsigned va = act ? vals + 8u * rank : scratch;
-        sh_st_f64(va, __dadd_rn(sh_ld_f64(va), __dmul_rn(at, v)));
+        sh_stv(va, Arith<V>::add(sh_ldv<V>(va), Arith<V>::mul(at, v)));
       });
       __syncwarp();
-      double* ov = a.out_val + o;
-      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ld_f64(vals + 8u * p);
+      V* ov = vcast<V>(a.out_val) + o;
+      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
       for (int sl = 0; sl < nslot; ++sl) sh_st(bits + 4u * (unsigned(sl) * 32u + lane), 0u);
       for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
@@ -1011,7 +1024,9 @@ template <int MODE>
 static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
   const BwLayout L = bw_layout(MODE, a.bw_wmax, a.bw_vmax, a.bw_bmax);
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
-  auto kern = i32 ? k_bwrow<MODE, int> : k_bwrow<MODE, int64_t>;
+  const bool f32 = a.f32 && (MODE == MODE_FILL || MODE == MODE_DENSE);
+  auto kern = f32 ? (i32 ? k_bwrow<MODE, int, float> : k_bwrow<MODE, int64_t, float>)
+                  : (i32 ? k_bwrow<MODE, int, double> : k_bwrow<MODE, int64_t, double>);
   int best_nw = 1, best_warps = 0;
   for (int nw = 8; nw >= 1; nw >>= 1) {
     const size_t bytes = size_t(nw) * L.bytes;
@@ -1042,7 +1057,7 @@ constexpr int kBs2Slots = 16;
 template <typename IT, bool FILL>
 static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
   const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots, FILL, a.bw_vmax);
-  auto kern = k_bw_struct2<IT, FILL>;
+  auto kern = (FILL && a.f32) ? k_bw_struct2<IT, FILL, float> : k_bw_struct2<IT, FILL, double>;
   constexpr int nw = 8;
   const size_t bytes = size_t(nw) * L.bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

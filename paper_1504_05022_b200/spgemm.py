@@ -30,15 +30,16 @@ class DeviceCsr:
         return int(self.ci.numel())
 
     @staticmethod
-    def from_host(M, device="cuda", pin: bool = False) -> "DeviceCsr":
-        """Copy a host CSR (anything with .shape/.rp/.ci/.val numpy arrays) to the device."""
+    def from_host(M, device="cuda", pin: bool = False, dtype=torch.float64) -> "DeviceCsr":
+        """Copy a host CSR (anything with .shape/.rp/.ci/.val numpy arrays) to the device;
+        dtype=torch.float32 for SpSGEMM values."""
         def t(a, dt):
             x = torch.from_numpy(a).to(dt)
             if pin:
                 x = x.pin_memory()
             return x.to(device, non_blocking=pin)
         return DeviceCsr(int(M.shape[0]), int(M.shape[1]), t(M.rp, torch.int64), t(M.ci, torch.int32),
-                         t(M.val, torch.float64))
+                         t(M.val, dtype))
 
     def to_host(self):
         return (self.rp.cpu().numpy(), self.ci.cpu().numpy(), self.val.cpu().numpy())
@@ -56,9 +57,9 @@ def _ptr(t: torch.Tensor | None, dtype: torch.dtype, name: str) -> int | None:
     return t.data_ptr() if t.numel() > 0 else None
 
 
-def _csr_ptrs(M: DeviceCsr, name: str):
+def _csr_ptrs(M: DeviceCsr, name: str, vdtype=torch.float64):
     return (_ptr(M.rp, torch.int64, name + ".rp"), _ptr(M.ci, torch.int32, name + ".ci"),
-            _ptr(M.val, torch.float64, name + ".val"))
+            _ptr(M.val, vdtype, name + ".val"))
 
 
 def _stream_handle(stream) -> int | None:
@@ -146,9 +147,12 @@ class SpGEMM:
         self.A, self.B = A, B  # keep the inputs alive for the handle's lifetime
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self.h = ctypes.c_void_p()
-        ap, bp = _csr_ptrs(A, "A"), _csr_ptrs(B, "B")
-        check(self.lib.spgemm_create(ctypes.byref(self.h), A.rows, A.cols, B.cols, ap[0], ap[1], ap[2], A.nnz,
-                                     bp[0], bp[1], bp[2], B.nnz, _stream_handle(self.stream), flags))
+        self.f32 = A.val.dtype == torch.float32  # SpSGEMM (spgemm_create_f32)
+        vdt = torch.float32 if self.f32 else torch.float64
+        ap, bp = _csr_ptrs(A, "A", vdt), _csr_ptrs(B, "B", vdt)
+        create = self.lib.spgemm_create_f32 if self.f32 else self.lib.spgemm_create
+        check(create(ctypes.byref(self.h), A.rows, A.cols, B.cols, ap[0], ap[1], ap[2], A.nnz,
+                     bp[0], bp[1], bp[2], B.nnz, _stream_handle(self.stream), flags))
         self.nnz_c = None
 
     def symbolic(self) -> int:
@@ -162,12 +166,14 @@ class SpGEMM:
         if self.nnz_c is None:
             raise SpgemmError(5, "numeric before symbolic")
         dev = self.A.rp.device
+        vdt = torch.float32 if self.f32 else torch.float64
         if c_rp is None:
             c_rp = torch.empty(self.A.rows + 1, dtype=torch.int64, device=dev)
             c_ci = torch.empty(self.nnz_c, dtype=torch.int32, device=dev)
-            c_val = torch.empty(self.nnz_c, dtype=torch.float64, device=dev)
-        check(self.lib.spgemm_numeric(self.h, _ptr(c_rp, torch.int64, "c_rp"), _ptr(c_ci, torch.int32, "c_ci"),
-                                      _ptr(c_val, torch.float64, "c_val")), self.h)
+            c_val = torch.empty(self.nnz_c, dtype=vdt, device=dev)
+        numeric = self.lib.spgemm_numeric_f32 if self.f32 else self.lib.spgemm_numeric
+        check(numeric(self.h, _ptr(c_rp, torch.int64, "c_rp"), _ptr(c_ci, torch.int32, "c_ci"),
+                      _ptr(c_val, vdt, "c_val")), self.h)
         return DeviceCsr(self.A.rows, self.B.cols, c_rp, c_ci, c_val)
 
     def stats(self) -> dict:

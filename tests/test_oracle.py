@@ -371,3 +371,48 @@ def test_validate_csr():
     rp = A.rp.copy()
     rp[3] = rp[2] - 1
     assert oracle.validate_csr(25, 25, rp, A.ci) == 2
+
+
+# ---------------------------------------------------------------- SpSGEMM (fp32) fill
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (17, 9, 23), (64, 64, 64)])
+def test_f32_dense_bruteforce(shape, density):
+    """SpSGEMM oracle [P:403]: with integer values ±[1,8] every product and partial sum is an
+    integer below 2^24, exact in float32 — pattern and values equal the dense product."""
+    m, k, n = shape
+    A = gen.random_csr(m, k, density, 300 + m, mode="int", zero_frac=0.1)
+    B = gen.random_csr(k, n, density, 400 + n, mode="int", zero_frac=0.1)
+    R = oracle.spgemm(A, B, fp32=True)
+    assert R.val.dtype == np.float32
+    pat = (A.pattern_dense().astype(np.int64) @ B.pattern_dense().astype(np.int64)) > 0
+    np.testing.assert_array_equal(res_pattern(R, (m, n)), pat)
+    np.testing.assert_array_equal(res_dense(R, (m, n)), A.to_dense() @ B.to_dense())
+
+
+def test_f32_error_bound_and_pow2():
+    """Real fp32 values: |fl32(c) - c| <= gamma_{t+1}·Σ|a||b| with u = 2^-24 and t the
+    entry's number of products (product rounding + t-1 additions; the exact c from the
+    float64 dense product of the same fp32-rounded inputs) — a dropped or misordered term
+    fails this at the sizes used; and power-of-two scaling commutes bit for bit."""
+    m, k, n = 40, 300, 50
+    A = gen.random_csr(m, k, 0.3, 31, mode="real")
+    B = gen.random_csr(k, n, 0.3, 32, mode="real")
+    A32 = gen.Csr(A.shape, A.rp, A.ci, A.val.astype(np.float32).astype(np.float64))
+    B32 = gen.Csr(B.shape, B.rp, B.ci, B.val.astype(np.float32).astype(np.float64))
+    R = oracle.spgemm(A32, B32, fp32=True)
+    exact = A32.to_dense() @ B32.to_dense()          # float64: within 2^-53-scale of exact
+    terms = A32.pattern_dense().astype(np.int64) @ B32.pattern_dense().astype(np.int64)
+    got = res_dense(R, (m, n))
+    pat = res_pattern(R, (m, n))
+    bound = np.abs(A32.to_dense()) @ np.abs(B32.to_dense())
+    u = 2.0 ** -24
+    gam = (terms + 1) * u / (1 - (terms + 1) * u)
+    err = np.abs(got - exact)[pat]
+    assert np.all(err <= (gam * bound)[pat] + 1e-12 * bound[pat])
+    assert np.any(err > 0)                               # genuinely single precision
+    rowsA = np.repeat(np.arange(m), np.diff(A32.rp))
+    d1 = np.ldexp(1.0, (np.arange(m) % 7) - 3)
+    As = gen.Csr(A32.shape, A32.rp, A32.ci, A32.val * d1[rowsA])
+    Rs = oracle.spgemm(As, B32, fp32=True)
+    rows = np.repeat(np.arange(m), np.diff(R.rp))
+    np.testing.assert_array_equal(Rs.val, (R.val.astype(np.float64) * d1[rows]).astype(np.float32))

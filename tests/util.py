@@ -6,12 +6,13 @@ import oracle
 TOL = 1e-12  # north star: |Δc_ij| <= 1e-12 · Σ_k |a_ik||b_kj|
 
 
-def run_gpu(A, B, flags=0, stats=False):
+def run_gpu(A, B, flags=0, stats=False, fp32=False):
     import torch
 
     import paper_1504_05022_b200 as sg
-    dA = sg.DeviceCsr.from_host(A)
-    dB = dA if B is A else sg.DeviceCsr.from_host(B)
+    dt = torch.float32 if fp32 else torch.float64
+    dA = sg.DeviceCsr.from_host(A, dtype=dt)
+    dB = dA if B is A else sg.DeviceCsr.from_host(B, dtype=dt)
     op = sg.SpGEMM(dA, dB, flags)
     nnz = op.symbolic()
     C = op.numeric()
