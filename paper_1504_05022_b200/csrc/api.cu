@@ -681,7 +681,6 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
         if (h->tier_count[t] == 0) continue;
         Stage3Args a{};
         a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
-    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;
@@ -711,7 +710,6 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
       if (h->nlong > 0) {
         Stage3Args a{};
         a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
-    a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
         a.A = h->A;
         a.B = h->B;
         a.b_nnz = h->b_nnz;

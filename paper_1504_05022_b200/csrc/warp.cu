@@ -201,19 +201,19 @@ __device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci,
           }
         }
 #pragma unroll
-        for (int u = 0; u < kGroup; ++u) op(c[u], VALS ? v[u] : 0.0, VALS ? at[u] : 0.0, act[u]);
+        for (int u = 0; u < kGroup; ++u) op(c[u], VALS ? v[u] : V(0), VALS ? at[u] : V(0), act[u]);
       }
     } else {
       for (int t = 0; t < nE; ++t) {
         int4 r;
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(stage + 16u * t) : "memory");
-        const double at = VALS ? __hiloint2double(r.w, r.z) : 0.0;
+        const V at = VALS ? rec_val<V>(r) : V(0);  // fp64: both words; fp32: the low word
         for (int q0 = 0; q0 < r.y; q0 += 32) {
           const bool act = q0 + lane < r.y;
           const int q = r.x + q0 + lane;
           const int c = act ? __ldg(bci + q) : kEmptyKey;
-          const double v = (VALS && act) ? __ldg(bval + q) : 0.0;
+          const V v = (VALS && act) ? __ldg(bval + q) : V(0);
           op(c, v, at, act);
         }
       }
