@@ -463,6 +463,8 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
         "stage_ms": {n: [round(x, 4) for x in st["stage_ms"]] for n, st, _, _, _ in info},
         "class_ms": {n: {c: round(v["ms"], 3) for c, v in st["classes"].items() if v["ms"] > 0}
                      for n, st, _, _, _ in info},
+        "class_ms_symbolic": {n: {c: round(v["ms_symbolic"], 3) for c, v in st["classes"].items()
+                                  if v["ms_symbolic"] > 0} for n, st, _, _, _ in info},
         "gpu_launches": launches * steps,
         "clocks": clocks,
     }

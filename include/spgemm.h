@@ -91,6 +91,8 @@ typedef struct spgemm_stats {
   int64_t tier_c_entries[SPGEMM_NUM_TIERS];/* sum nnz(c_i*) over the rows of each class     */
   int32_t launches_symbolic;               /* kernels launched by the last symbolic         */
   int32_t launches_numeric;                /* kernels launched by the last numeric          */
+  float tier_ms_symbolic[SPGEMM_NUM_TIERS];/* stage-3 time per class in the last symbolic
+                                              (PRECISE: the COUNT / STRUCT pass)             */
 } spgemm_stats_t;
 
 /* Create a handle for C = A·B.  No device work, no synchronisation (unless VALIDATE).

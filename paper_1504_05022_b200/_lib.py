@@ -45,14 +45,16 @@ class SpgemmStats(ctypes.Structure):
         ("tier_c_entries", ctypes.c_int64 * NUM_TIERS),
         ("launches_symbolic", ctypes.c_int32),
         ("launches_numeric", ctypes.c_int32),
+        ("tier_ms_symbolic", ctypes.c_float * NUM_TIERS),
     ]
 
     def as_dict(self) -> dict:
-        arrays = ("tier_rows", "stage_ms", "tier_ms", "tier_a_entries", "tier_products", "tier_c_entries")
+        arrays = ("tier_rows", "stage_ms", "tier_ms", "tier_ms_symbolic", "tier_a_entries", "tier_products", "tier_c_entries")
         d = {f: getattr(self, f) for f, _ in self._fields_ if f not in arrays}
         d["tier_rows"] = {TIER_NAMES[t]: int(self.tier_rows[t]) for t in range(NUM_TIERS) if self.tier_rows[t]}
         d["stage_ms"] = [float(x) for x in self.stage_ms]
         d["classes"] = {TIER_NAMES[t]: dict(rows=int(self.tier_rows[t]), ms=float(self.tier_ms[t]),
+                                            ms_symbolic=float(self.tier_ms_symbolic[t]),
                                             a_entries=int(self.tier_a_entries[t]),
                                             products=int(self.tier_products[t]),
                                             c_entries=int(self.tier_c_entries[t]))

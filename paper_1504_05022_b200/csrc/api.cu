@@ -28,7 +28,8 @@ thread_local int64_t* t_pinned = nullptr;  // small pinned scratch for the count
 struct EventSet {
   int device;
   cudaEvent_t ev[6];
-  cudaEvent_t tev[NUM_TIERS][2];
+  cudaEvent_t tev[NUM_TIERS][2];   // stage-3 classes of the last numeric (precise) / symbolic (hybrid)
+  cudaEvent_t tsym[NUM_TIERS][2];  // stage-3 classes of the last symbolic
 };
 thread_local std::vector<EventSet*> t_event_pool;
 int g_force_tier = -1;
@@ -139,7 +140,9 @@ struct spgemm_handle_s {
   EventSet* evs = nullptr;
   cudaEvent_t* ev = nullptr;
   cudaEvent_t (*tev)[2] = nullptr;
+  cudaEvent_t (*tsym)[2] = nullptr;
   bool tev_used[NUM_TIERS] = {};
+  bool tsym_used[NUM_TIERS] = {};
   int32_t launches_sym = 0, launches_num = 0;
   bool ev_ok = false;
   bool numeric_recorded = false;
@@ -439,10 +442,14 @@ spgemm_status_t spgemm_create(spgemm_handle_t* handle, int64_t m, int64_t k, int
     h->evs->device = h->device;
     for (int i = 0; i < 6; ++i) cudaEventCreate(&h->evs->ev[i]);
     for (int t = 0; t < NUM_TIERS; ++t)
-      for (int i = 0; i < 2; ++i) cudaEventCreate(&h->evs->tev[t][i]);
+      for (int i = 0; i < 2; ++i) {
+        cudaEventCreate(&h->evs->tev[t][i]);
+        cudaEventCreate(&h->evs->tsym[t][i]);
+      }
   }
   h->ev = h->evs->ev;
   h->tev = h->evs->tev;
+  h->tsym = h->evs->tsym;
   h->ev_ok = true;
   if (flags & SPGEMM_FLAG_VALIDATE) {
     int32_t* err = nullptr;
@@ -509,7 +516,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   CK(h, cudaMemsetAsync(h->nnz_row, 0, sizeof(int64_t) * m, h->stream));
   TierParams tp{g_force_tier, g_long_threshold};
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
-  for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = false;
+  for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = h->tsym_used[t] = false;
   // C~ offsets in both strategies: hybrid keeps whole rows there, precise only the sorted
   // column sets of the window-bitmap rows (4 B/entry) for its numeric pass
   const int cap_mode = precise ? CAP_PRECISE : CAP_HYBRID;
@@ -563,16 +570,16 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
       AL(h, &a.bw_ovf_list, h->tier_count[T_BW]);
       AL(h, &a.bw_ovf_cnt, 1);
     }
-    cudaEventRecord(h->tev[t][0], h->stream);
+    cudaEventRecord(h->tsym[t][0], h->stream);
     CK(h, launch_stage3_tier(t, a, h->stream));
-    cudaEventRecord(h->tev[t][1], h->stream);
-    h->tev_used[t] = true;
+    cudaEventRecord(h->tsym[t][1], h->stream);
+    h->tsym_used[t] = true;
     ++h->launches_sym;
   }
   tr("stage 3 classes");
   h->nlong = h->tier_count[T_LONG];
   h->long_first = h->tier_off[T_LONG];
-  if (h->nlong > 0) cudaEventRecord(h->tev[T_LONG][0], h->stream);
+  if (h->nlong > 0) cudaEventRecord(h->tsym[T_LONG][0], h->stream);
   if (hybrid) {
     // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297]; the
     // rows' sorted results (values in the oracle's order) are their C~ slices in the long-row
@@ -600,8 +607,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->launches_sym += 1;
   }
   if (h->nlong > 0) {
-    cudaEventRecord(h->tev[T_LONG][1], h->stream);
-    h->tev_used[T_LONG] = true;
+    cudaEventRecord(h->tsym[T_LONG][1], h->stream);
+    h->tsym_used[T_LONG] = true;
   }
   cudaEventRecord(h->ev[2], h->stream);
   // stage 4 (first half): sum the numbers of nonzero entries of all rows [P:301]
@@ -799,11 +806,18 @@ spgemm_status_t spgemm_get_stats(spgemm_handle_t h, spgemm_stats_t* out) {
       cudaEventSynchronize(h->ev[5]);
       cudaEventElapsedTime(&out->stage_ms[3], h->ev[4], h->ev[5]);
     }
-    for (int t = 0; t < NUM_TIERS; ++t)
-      if (h->tev_used[t]) {
+    const bool precise = (h->flags & SPGEMM_FLAG_PRECISE) != 0;
+    for (int t = 0; t < NUM_TIERS; ++t) {
+      if (h->tsym_used[t]) {
+        cudaEventSynchronize(h->tsym[t][1]);
+        cudaEventElapsedTime(&out->tier_ms_symbolic[t], h->tsym[t][0], h->tsym[t][1]);
+        if (!precise) out->tier_ms[t] = out->tier_ms_symbolic[t];
+      }
+      if (precise && h->tev_used[t]) {
         cudaEventSynchronize(h->tev[t][1]);
         cudaEventElapsedTime(&out->tier_ms[t], h->tev[t][0], h->tev[t][1]);
       }
+    }
     out->launches_symbolic = h->launches_sym;
     out->launches_numeric = h->launches_num;
     if (h->m > 0) {
