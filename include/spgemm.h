@@ -163,6 +163,13 @@ spgemm_status_t spgemm_set_debug(int32_t force_tier, int64_t long_initial_capaci
  * Errors: INVALID_VALUE (negative). */
 spgemm_status_t spgemm_set_debug_long_tile(int64_t tile_columns);
 
+/* Debug / test knob: precise numeric sends long rows whose column window is wider than
+ * min_window columns (and whose u_i <= 2^20) to the bucket path — a stable partition of the
+ * row's products by column range, then one CTA sort per bucket (the ESC of [P:277-284] over
+ * column ranges) — instead of the bitmap rank kernel.  0 = default (2^18, one rank tile),
+ * negative = never.  Takes effect at the next spgemm_symbolic.  Process-wide; not thread-safe. */
+spgemm_status_t spgemm_set_debug_long_bucket(int64_t min_window);
+
 /* Workspace comes from a library-owned stream-ordered memory pool per device that keeps
  * freed blocks cached (warm multiplies make no OS allocations; the device's default pool and
  * PyTorch's allocator are not touched).  This returns cached bytes above keep_bytes to the

@@ -126,6 +126,8 @@ def load():
     lib.spgemm_set_debug.argtypes = [ctypes.c_int32, I64, I64]
     lib.spgemm_set_debug_long_tile.restype = st
     lib.spgemm_set_debug_long_tile.argtypes = [I64]
+    lib.spgemm_set_debug_long_bucket.restype = st
+    lib.spgemm_set_debug_long_bucket.argtypes = [I64]
     lib.spgemm_trim_workspace_cache.restype = st
     lib.spgemm_trim_workspace_cache.argtypes = [I64]
     lib.spgemm_status_string.restype = ctypes.c_char_p

@@ -35,6 +35,7 @@ thread_local std::vector<EventSet*> t_event_pool;
 int g_force_tier = -1;
 int64_t g_long_cap0 = 16384;
 int64_t g_long_threshold = 0;
+int64_t g_bk_min_w = kBkDefaultMinW;  // long rows: bucket path above this window (precise numeric)
 
 __global__ void k_tier_to_i32(const uint8_t* t, int32_t* o, int64_t m) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -144,6 +145,8 @@ struct spgemm_handle_s {
   bool tev_used[NUM_TIERS] = {};
   bool tsym_used[NUM_TIERS] = {};
   int32_t launches_sym = 0, launches_num = 0;
+  int64_t bk_min_w = kBkDefaultMinW;  // precise long rows: bucket-path window threshold (at symbolic)
+  int64_t bk_u = 0, bk_rows = 0;      // sum u and number of the long rows on the bucket path
   bool ev_ok = false;
   bool numeric_recorded = false;
 };
@@ -385,6 +388,11 @@ spgemm_status_t spgemm_set_debug(int32_t force_tier, int64_t long_initial_capaci
   return SPGEMM_SUCCESS;
 }
 
+spgemm_status_t spgemm_set_debug_long_bucket(int64_t min_window) {
+  g_bk_min_w = min_window == 0 ? kBkDefaultMinW : (min_window < 0 ? INT64_MAX : min_window);
+  return SPGEMM_SUCCESS;
+}
+
 spgemm_status_t spgemm_set_debug_long_tile(int64_t tile_columns) {
   if (tile_columns < 0) return fail(nullptr, SPGEMM_ERROR_INVALID_VALUE, "negative tile width");
   g_long_tile_words = (tile_columns + 31) / 32;
@@ -514,7 +522,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
   // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
   CK(h, cudaMemsetAsync(h->nnz_row, 0, sizeof(int64_t) * m, h->stream));
-  TierParams tp{g_force_tier, g_long_threshold};
+  TierParams tp{g_force_tier, g_long_threshold, g_bk_min_w};
+  h->bk_min_w = g_bk_min_w;
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = h->tsym_used[t] = false;
   // C~ offsets in both strategies: hybrid keeps whole rows there, precise only the sorted
@@ -638,6 +647,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     h->long_first = h->tier_off[T_LONG];
     h->bw_vmax = h->pinned[kSumVmax];  // exact: max nnz(c_i*) over the window rows
     h->bw_bmax = h->pinned[kSumBmax];
+    h->bk_u = h->pinned[kSumBkU];
+    h->bk_rows = h->pinned[kSumBkRows];
   }
   h->sym_ok = true;
   *c_nnz = h->nnz_c;
@@ -729,9 +740,31 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
         a.out_val = c_val;
         a.mode = MODE_FILL;
         a.bwin = h->ws.bwin;
+        a.rlo = h->ws.rlo;
+        a.rhi = h->ws.rhi;
+        a.U = h->ws.U;
         a.work_ctr = h->work_ctr;
         cudaEventRecord(h->tev[T_LONG][0], h->stream);
-        CK(h, launch_long_bitmap(a, h->stream));
+        if (h->bk_rows > 0) {
+          // wide windows: bucket partition + per-bucket sort (longbk.cu); the rest: rank kernel.
+          // Workspace for this call only (stream-ordered pool, freed after the launches).
+          const int64_t ndesc = h->bk_u / 1024 + h->bk_rows;
+          const size_t vb = vbytes(h);
+          const size_t sz[7] = {sizeof(int32_t) * size_t(h->bk_u), vb * size_t(h->bk_u), sizeof(BkDesc) * size_t(ndesc),
+                                sizeof(BkRow) * size_t(h->bk_rows), 2 * sizeof(unsigned long long),
+                                2 * sizeof(int32_t), sizeof(int32_t) * size_t(h->nlong)};
+          void* p[7] = {};
+          for (int q = 0; q < 7; ++q) CK(h, pool_malloc(&p[q], sz[q], h->stream));
+          BkWork bw{static_cast<int32_t*>(p[0]), static_cast<double*>(p[1]), static_cast<BkDesc*>(p[2]),
+                    static_cast<BkRow*>(p[3]), static_cast<unsigned long long*>(p[4]), static_cast<int32_t*>(p[5]),
+                    static_cast<int32_t*>(p[6]), h->bk_min_w};
+          const cudaError_t e = launch_long_buckets(a, bw, h->bk_rows, h->stream);
+          for (int q = 0; q < 7; ++q) cudaFreeAsync(p[q], h->stream);
+          CK(h, e);
+          h->launches_num += 4;
+        } else {
+          CK(h, launch_long_bitmap(a, h->stream));
+        }
         cudaEventRecord(h->tev[T_LONG][1], h->stream);
         h->tev_used[T_LONG] = true;
         ++h->launches_num;

@@ -53,7 +53,31 @@ __host__ __device__ inline bool bw_ok(int64_t cap, int64_t W) {
 struct TierParams {
   int force_tier;         // -1 = off
   int64_t long_threshold; // rows with cap above go long (0 = default by smem)
+  int64_t bk_min_w;       // precise long rows: window above which values take the bucket path
 };
+
+// Long rows, precise numeric: rows whose column window is wider than one bitmap tile of the
+// rank kernel (W > bk_min_w) and whose products fit the bucket count take the bucket path
+// (longbk.cu): a stable partition of the row's products by column range, then one CTA sort per
+// bucket.  Products per bucket: ~kBkTarget on average, at most kBkCap (else the row falls back
+// to the rank kernel).
+constexpr int64_t kBkDefaultMinW = int64_t(1) << 18;
+constexpr int kBkTarget = 2048;
+constexpr int kBkCap = 4096;
+constexpr int kBkMaxBuckets = 512;
+__host__ __device__ inline bool bk_eligible(int64_t u, int64_t W, int64_t min_w) {
+  return W > min_w && u <= int64_t(kBkTarget) * kBkMaxBuckets;
+}
+// buckets: NB = next power of two >= ceil(u / kBkTarget); bucket of column c = (c - lo) >> sh,
+// sh = max(0, ceil(log2 W) - log2 NB); ((W - 1) >> sh) + 1 <= NB buckets are used
+__host__ __device__ inline void bk_shape(int64_t u, int64_t W, int& sh, int& nbk) {
+  int lnb = 0;
+  while ((int64_t(kBkTarget) << lnb) < u) ++lnb;
+  int lw = 0;
+  while ((int64_t(1) << lw) < W) ++lw;
+  sh = lw > lnb ? lw - lnb : 0;
+  nbk = (int)(((W - 1) >> sh) + 1);
+}
 
 __host__ __device__ inline int tier_capacity_ok(int t, int64_t u, int64_t cap, int64_t W) {
   if (t == T_EMPTY) return u == 0;
@@ -203,6 +227,8 @@ struct Stage3Args {
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
   const int32_t* rlo;         // first column of each row's window (stage 1)
+  const int32_t* rhi;         // last column of each row's window (stage 1)
+  const int64_t* U;           // u_i of every row (stage 1)
   const int4* bwin;           // (first, last, nnz) of each row of B (stage 1)
   int64_t bw_wmax, bw_vmax;   // T_BW: largest window / row length of the class
   int64_t bw_bmax;            // T_BW numeric: most nonzero 1024-column blocks in a row
@@ -240,6 +266,7 @@ struct Stage12Ws {
   int64_t* summary;    // [kSumLen] device
   int4* bwin;          // [k] (first column, last column, nnz, 0) of each row of B
   int32_t* rlo;        // [m] first column of each row's window
+  int32_t* rhi;        // [m] last column of each row's window
   int64_t nblk;
 };
 constexpr int kS12Threads = 256;
@@ -255,7 +282,9 @@ constexpr int kSumWmax = kSumU + 3;              // max W over T_BW rows
 constexpr int kSumVmax = kSumU + 4;              // max min(u, W) over T_BW rows (after re-binning:
                                                  // max nnz(c_i*))
 constexpr int kSumBmax = kSumU + 5;              // max nonzero 1024-column blocks (T_BW STRUCT)
-constexpr int kSumLen = kSumU + 6;
+constexpr int kSumBkU = kSumU + 6;               // precise long rows on the bucket path: sum u
+constexpr int kSumBkRows = kSumU + 7;            //   and their number
+constexpr int kSumLen = kSumU + 8;
 
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           int cap_mode, Stage12Ws& ws, cudaStream_t s);
@@ -276,6 +305,29 @@ cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s);
 cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s);
 // PRECISE long rows: bitmap over the column window (COUNT: nnz; FILL: ranks → C)
 cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s);
+// long rows with wide windows, precise numeric: bucket partition + per-bucket sort (longbk.cu)
+struct BkDesc {      // one bucket of one row
+  int64_t off;       // its first item in the staging arrays
+  int32_t size;      // items (products)
+  int32_t blo;       // first column of its column range
+  int32_t sh;        // key bits (the range is 2^sh columns)
+  int32_t uniq;      // distinct columns (written by the sort)
+};
+struct BkRow {       // one row on the bucket path: buckets [desc0, desc0 + nbk)
+  int32_t row, nbk;
+  int64_t desc0;
+};
+struct BkWork {
+  int32_t* stg_col;          // staging: sum u over the bucket rows
+  double* stg_val;           //   (fp64, or fp32 reinterpreted)
+  BkDesc* desc;
+  BkRow* rows;
+  unsigned long long* cur64; // [0] staging items used, [1] descriptors used
+  int32_t* cur32;            // [0] bucket rows, [1] rows left to the rank kernel
+  int32_t* fb_list;          // those rows
+  int64_t min_w;             // bk_eligible window threshold
+};
+cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t max_rows, cudaStream_t s);
 
 // Exclusive scan of int64 values x[0..len) into y[0..len]; y[len] = total.  tmp must hold
 // scan_tmp_elems(len) int64.

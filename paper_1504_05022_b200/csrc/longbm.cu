@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
   __shared__ int64_t s_next;
   __shared__ int64_t s_tab[PROG ? kMaxChunks : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t r = blockIdx.x; r < a.count; r = next_row(a, r, &s_next)) {
+  const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;  // fallback lists: on the device
+  for (int64_t r = blockIdx.x; r < count; r = next_row(a, r, &s_next)) {
     const int k_long = PROG ? __ldg(a.active + r) : 0;
     const int row = __ldg(a.perm + a.first + (PROG ? int64_t(k_long) : r));
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);

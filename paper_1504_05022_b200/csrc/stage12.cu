@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
                                                const int4* __restrict__ bwin, TierParams tp,
                                                int cap_mode, int64_t* __restrict__ U,
                                                uint8_t* __restrict__ tier, int32_t* __restrict__ rlo,
+                                               int32_t* __restrict__ rhi,
                                                int32_t* __restrict__ blk_tier,
                                                int64_t* __restrict__ blk_cap,
                                                int64_t* __restrict__ blk_usum,
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
       U[i] = u;
       tier[i] = (uint8_t)t;
       rlo[i] = lo;
+      rhi[i] = hi;
       atomicAdd(&s_hist[t], 1);
       capsum += ctil_capacity(cap_mode, t, u, n);
       usum += u;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
 template <int NT, int RPT>
 __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_t* __restrict__ U,
                                               const int64_t* __restrict__ nnz_row, TierParams tp,
+                                              const int32_t* __restrict__ rlo, const int32_t* __restrict__ rhi,
                                               uint8_t* __restrict__ tier, int32_t* __restrict__ blk_tier,
                                               int64_t* __restrict__ blk_cap, int64_t* __restrict__ blk_usum,
                                               int64_t* __restrict__ blk_umax, int64_t* __restrict__ summary) {
@@ -188,6 +191,7 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * NT * RPT;
   int64_t vmax = 0;
+  unsigned long long bku = 0, bkr = 0;  // long rows on the bucket path (longbk.cu)
   for (int r = 0; r < RPT; ++r) {
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     if (i < m) {
@@ -195,7 +199,20 @@ __global__ void __launch_bounds__(NT) k_rebin(int64_t m, int64_t n, const int64_
       tier[i] = (uint8_t)t;
       atomicAdd(&s_hist[t], 1);
       if (t == T_BW) vmax = nnz_row[i] > vmax ? nnz_row[i] : vmax;
+      if (t == T_LONG && bk_eligible(U[i], int64_t(rhi[i]) - rlo[i] + 1, tp.bk_min_w)) {
+        bku += (unsigned long long)U[i];
+        ++bkr;
+      }
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bku += __shfl_xor_sync(0xffffffffu, bku, o);
+    bkr += __shfl_xor_sync(0xffffffffu, bkr, o);
+  }
+  if ((threadIdx.x & 31) == 0 && bkr > 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(summary + kSumBkU), bku);
+    atomicAdd(reinterpret_cast<unsigned long long*>(summary + kSumBkRows), bkr);
   }
   // max nnz(c_i*) of the bw rows: one global atomic per block
 #pragma unroll
@@ -426,7 +443,7 @@ cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B,
   if (e != cudaSuccess) return e;
   if (k > 0) k_bwin<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, B.rp, B.ci, ws.bwin);
   k_stage1<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, A, B.rp, ws.bwin, tp, cap_mode, ws.U, ws.tier, ws.rlo, ws.blk_tier, ws.blk_cap,
+      m, n, A, B.rp, ws.bwin, tp, cap_mode, ws.U, ws.tier, ws.rlo, ws.rhi, ws.blk_tier, ws.blk_cap,
       ws.blk_usum, ws.blk_umax, ws.summary);
   return cudaGetLastError();
 }
@@ -446,8 +463,10 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
   if (m == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(ws.summary + kSumVmax, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ws.summary + kSumBkU, 0, 2 * sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
   k_rebin<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, ws.U, nnz_row, tp, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax, ws.summary);
+      m, n, ws.U, nnz_row, tp, ws.rlo, ws.rhi, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax, ws.summary);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_stage2(m, ws, CAP_NONE, n, s);

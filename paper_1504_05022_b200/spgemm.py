@@ -73,6 +73,13 @@ def set_debug(force_tier: int = -1, long_initial_capacity: int = 0, long_thresho
     check(lib.spgemm_set_debug(force_tier, long_initial_capacity, long_threshold))
 
 
+def set_debug_long_bucket(min_window: int = 0):
+    """Test knob: long rows with column windows wider than `min_window` take the bucket path
+    in precise numeric (0 = default 2^18, negative = never).  See spgemm_set_debug_long_bucket."""
+    lib = load()
+    check(lib.spgemm_set_debug_long_bucket(int(min_window)))
+
+
 def set_debug_long_tile(tile_columns: int = 0):
     """Testing knob: long-row bitmap tiles of at most tile_columns columns (0 = default)."""
     lib = load()

@@ -25,9 +25,11 @@ def _reset_debug():
     import paper_1504_05022_b200 as sg
     sg.set_debug(-1, 0, 0)
     sg.set_debug_long_tile(0)
+    sg.set_debug_long_bucket(0)
     yield
     sg.set_debug(-1, 0, 0)
     sg.set_debug_long_tile(0)
+    sg.set_debug_long_bucket(0)
 
 
 def _dense_csr(D, pattern=None):
@@ -473,3 +475,44 @@ def test_warp_classes_crowded_window(flags_name, mode):
     np.testing.assert_array_equal(g["rp"], R.rp)
     np.testing.assert_array_equal(g["ci"], R.ci)
     np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+
+
+@pytest.mark.parametrize("mode", ["int", "real"])
+@pytest.mark.parametrize("min_window", [1, 0])
+def test_long_bucket_path(mode, min_window):
+    """Precise long rows on the bucket path (longbk.cu): the row's products partitioned by
+    column range in product order, each bucket sorted stably and its runs summed left to right.
+    Rows: wide windows (2 Mi columns) with 8 Ki-60 Ki products; one row whose products crowd
+    one bucket past its capacity (fallback to the rank kernel); short-window rows (rank kernel
+    unless the knob sends every long row to the bucket path).  Structure exact, values bit for
+    bit against the oracle and run to run."""
+    import paper_1504_05022_b200 as sg
+    n = 1 << 21
+    lens = np.array([16, 64, 200, 400, 31, 5] * 500)[:3000]
+    B = gen.random_rows(3000, n, lens, seed=51, mode=mode)
+    # rows 3000..3039: crowded, all columns in [0, 6000)
+    Bc = gen.random_rows(40, 6000, np.full(40, 300), seed=52, mode=mode)
+    Bn = gen.random_rows(20, 50_000, np.full(20, 500), seed=53, mode=mode)  # short windows
+    rp = np.concatenate([B.rp, B.rp[-1] + Bc.rp[1:], B.rp[-1] + Bc.rp[-1] + Bn.rp[1:]])
+    Bfull = gen.Csr((3060, n), rp, np.concatenate([B.ci, Bc.ci, Bn.ci]), np.concatenate([B.val, Bc.val, Bn.val]))
+    rows, cols = [], []
+    for i in range(48):
+        if i < 40:
+            js = np.sort(np.unique((np.arange(40 + 8 * i) * 7919 + i * 31) % 3000))
+        elif i < 44:
+            js = np.array([0] + list(range(3000, 3040)))  # 12 000 products in [0, 6000) + a wide
+            #                                            b_0*: one bucket holds > kBkCap products
+        else:
+            js = np.arange(3040, 3060)             # 10 000 products, window 50 000
+        rows += [i] * len(js)
+        cols += list(js)
+    A = gen.with_values(gen.from_coo(np.array(rows), np.array(cols), (48, 3060)), mode, 54)
+    sg.set_debug_long_bucket(min_window)
+    g = run_gpu(A, Bfull, flags=sg.FLAG_PRECISE, stats=True)
+    g2 = run_gpu(A, Bfull, flags=sg.FLAG_PRECISE)
+    R = oracle.spgemm(A, Bfull)
+    assert g["stats"]["long_rows"] >= 40
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+    np.testing.assert_array_equal(g2["val"].view(np.int64), g["val"].view(np.int64))
