@@ -518,6 +518,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   AL(h, &ws.summary, kSumLen);
   AL(h, &ws.bwin, h->k > 0 ? h->k : 1);
   AL(h, &ws.rlo, m);
+  AL(h, &ws.rhi, m);
   AL(h, &h->nnz_row, m);
   AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
   // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
