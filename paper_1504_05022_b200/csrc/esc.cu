@@ -15,11 +15,13 @@
 // The warp classes' rows (u <= 2048) are sorted by a run merge instead (k_esc_merge below):
 // every b_j* is already sorted, so ⌈log2 runs⌉ stable pairwise merges sort the row.
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include <cub/block/block_radix_sort.cuh>
 
 #include "common.cuh"
+#include "esc_sort.cuh"
 
 namespace sg {
 
@@ -222,6 +224,109 @@ cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
   if (grid > a.count) grid = a.count;
   kern<<<(unsigned)grid, NT, bytes, s>>>(a);
   return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------
+// Bucket ESC (esc_sort.cuh): expand the row's products in product order, sort them by
+// (column, p) with one counting pass into ~32-product buckets plus warp bitonic sorts, sum the
+// runs left to right.  Replaces the block radix sort (4 passes over 22-bit keys on c3a) and the
+// run merge (log2(runs) rounds) for the warp and ESC classes.
+template <int NT, int CAP, typename IT, typename V>
+__global__ void __launch_bounds__(NT) k_esc_bk(Stage3Args a) {
+  constexpr int NW = NT / 32;
+  using SM = escs::Smem<CAP, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  __shared__ IT s_bs[NT];
+  __shared__ int s_len[NT], s_pex[NT];
+  __shared__ V s_av[NT];
+  __shared__ int s_w[NW + 1];
+  __shared__ unsigned s_max[NW];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+  const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;
+  const int64_t rper = (count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA
+  const int64_t rend = min(int64_t(blockIdx.x) * rper + rper, count);
+  for (int64_t r = int64_t(blockIdx.x) * rper; r < rend; ++r) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    // 1. expand (lines 3-6 of Algorithm 1): product p of the row at key/pval[p]
+    int u = 0;
+    unsigned kmax = 0;
+    for (int64_t e0 = a0; e0 < a1; e0 += NT) {
+      const int64_t e = e0 + tid;
+      int len = 0;
+      if (e < a1) {
+        const int j = __ldg(a.A.ci + e);
+        const int64_t b0 = __ldg(a.B.rp + j);
+        len = (int)(__ldg(a.B.rp + j + 1) - b0);
+        s_bs[tid] = (IT)b0;
+        s_av[tid] = __ldg(vcast<V>(a.A.val) + e);
+      }
+      int tot;
+      const int ex = escs::block_excl_scan<NT>(len, &tot, s_w);
+      s_len[tid] = len;
+      s_pex[tid] = u + ex;
+      __syncthreads();
+      const int na = (int)((a1 - e0) < NT ? (a1 - e0) : NT);
+      for (int t = w; t < na; t += NW) {
+        const IT bs = s_bs[t];
+        const int lt = s_len[t], pe = s_pex[t];
+        const V at = s_av[t];
+        for (int q = lane; q < lt; q += 32) {
+          const unsigned k = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
+          sm.key[pe + q] = k;
+          kmax = k > kmax ? k : kmax;
+          sm.pval[pe + q] = Arith<V>::mul(at, __ldg(vcast<V>(a.B.val) + bs + q));  // line 6
+        }
+      }
+      u += tot;
+      __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    if (lane == 0) s_max[w] = kmax;
+    __syncthreads();
+    unsigned km = 0;
+#pragma unroll
+    for (int x = 0; x < NW; ++x) km = s_max[x] > km ? s_max[x] : km;
+    const int kb = km ? 32 - __clz(km) : 0;
+    // 2. sort by (column, p); 3. compress into the row's output
+    const int pb = escs::sort_products<NT, CAP, V>(sm, u, kb);
+    const int64_t o = __ldg(a.out_off + row);
+    const int nnz = escs::compress_write<NT, CAP, V>(sm, u, pb, lo, a.out_col + o, vcast<V>(a.out_val) + o);
+    if (tid == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+    __syncthreads();
+  }
+}
+
+template <int NT, int CAP, typename IT, typename V>
+cudaError_t launch_bk_k(const Stage3Args& a, cudaStream_t s) {
+  const size_t bytes = sizeof(escs::Smem<CAP, V>);
+  auto kern = k_esc_bk<NT, CAP, IT, V>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = int64_t(num_sms()) * per_sm;
+  if (grid > a.count) grid = a.count;
+  kern<<<(unsigned)grid, NT, bytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT, int CAP>
+cudaError_t launch_bk_t(const Stage3Args& a, cudaStream_t s) {
+  const bool i32 = a.b_nnz < (int64_t(1) << 31);
+  if (a.f32) return i32 ? launch_bk_k<NT, CAP, int, float>(a, s) : launch_bk_k<NT, CAP, int64_t, float>(a, s);
+  return i32 ? launch_bk_k<NT, CAP, int, double>(a, s) : launch_bk_k<NT, CAP, int64_t, double>(a, s);
+}
+
+bool esc_old() {
+  static const bool v = getenv("SPGEMM_ESC_OLD") != nullptr;  // A/B switch (development)
+  return v;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -433,6 +538,15 @@ cudaError_t launch_merge_t(const Stage3Args& a, cudaStream_t s) {
 // merge (measured faster than the radix sort at these sizes; slower at 4096+, c3a / c5).
 cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
+  if (!esc_old()) switch (S) {
+    case 64: return launch_bk_t<32, 64>(a, s);
+    case 128: return launch_bk_t<32, 128>(a, s);
+    case 256: return launch_bk_t<64, 256>(a, s);
+    case 512: return launch_bk_t<64, 512>(a, s);
+    case 1024: return launch_bk_t<128, 1024>(a, s);
+    case 2048: return launch_bk_t<256, 2048>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
   switch (S) {
     case 64: return launch_merge_t<32, 3>(a, s);
     case 128: return launch_merge_t<32, 5>(a, s);
@@ -447,6 +561,12 @@ cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
 // e2048: run merge (5.9 vs 6.3 ms on c3a); e4096 / e8192: radix (merge 25.0 vs 21.1 ms)
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
+  if (!esc_old()) switch (tier) {
+    case T_E2048: return launch_bk_t<256, 2048>(a, s);
+    case T_E4096: return launch_bk_t<256, 4096>(a, s);
+    case T_E8192: return launch_bk_t<512, 8192>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
   switch (tier) {
     case T_E2048: return launch_merge_t<256, 9>(a, s);
     case T_E4096: return launch_esc_t<256, 16>(a, s);

@@ -16,17 +16,16 @@
 //              of every bucket in product order (j ascending, then k): a stable partition.
 //              Within one warp step the lanes hold one b_j*'s sorted columns, so the lanes of
 //              a bucket form one run: rank = lane - run start, no atomics.
-//   k_bk_sort  CTA per bucket: stable block radix sort over the bucket's sh key bits (items
-//              in product order, so equal columns stay in product order), runs of equal
+//   k_bk_sort  CTA per bucket: the bucket's products sorted by (column, p) (esc_sort.cuh:
+//              counting pass into ~32-product sub-buckets, warp bitonic sorts), runs of equal
 //              columns summed left to right (lines 9, 11: the oracle's order, bit for bit,
 //              DESIGN.md R1); the distinct entries overwrite the bucket's items.
 //   k_bk_copy  CTA per row: scan of its buckets' distinct counts, copy into C at row_ptr.
 // Rows that do not qualify (bk_eligible) or whose largest bucket exceeds kBkCap go to the
 // rank kernel (fallback list).
-#include <cub/block/block_radix_sort.cuh>
-
 #include "common.cuh"
 #include "walk.cuh"
+#include "esc_sort.cuh"
 
 namespace sg {
 
@@ -37,8 +36,7 @@ using walk::walk_row;
 
 constexpr int kPNT = 256;            // k_bk_part
 constexpr int kPNW = kPNT / 32;
-constexpr int kSNT = 256;            // k_bk_sort: kSNT x kSIPT = kBkCap items
-constexpr int kSIPT = kBkCap / kSNT;
+constexpr int kSNT = 256;            // k_bk_sort (kBkCap items per bucket)
 constexpr int kCNT = 256;            // k_bk_copy
 
 __device__ __forceinline__ unsigned lanemask_le_() {
@@ -191,80 +189,24 @@ __global__ void __launch_bounds__(kPNT) k_bk_part(Stage3Args a, BkWork bw) {
 
 // ------------------------------------------------------------------------------- bucket sort
 template <typename V>
-struct BkSortSmem {
-  using Sort = cub::BlockRadixSort<unsigned, kSNT, kSIPT, unsigned short, 6>;
-  union {
-    typename Sort::TempStorage sort;
-    unsigned key[kBkCap];
-  };
-  V val[kBkCap];   // the bucket's products in item order
-  V sval[kBkCap];  // the same, in sorted order
-};
-
-template <typename V>
 __global__ void __launch_bounds__(kSNT) k_bk_sort(BkWork bw) {
-  using SM = BkSortSmem<V>;
+  using SM = escs::Smem<kBkCap, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
-  __shared__ int s_w[kSNT / 32 + 1];
   const int tid = threadIdx.x;
   V* sv = vcast<V>(bw.stg_val);
   const int64_t nd = (int64_t)bw.cur64[1];
   for (int64_t d = blockIdx.x; d < nd; d += gridDim.x) {
     const BkDesc D = bw.desc[d];
     const int n = D.size;
-    if (n == 0) {
-      if (tid == 0) bw.desc[d].uniq = 0;
-      continue;
-    }
-    for (int i = tid; i < kBkCap; i += kSNT) {
-      sm.key[i] = i < n ? (unsigned)(bw.stg_col[D.off + i] - D.blo) : 0xffffffffu;  // pad sorts last
-      if (i < n) sm.val[i] = sv[D.off + i];
+    for (int i = tid; i < n; i += kSNT) {  // the bucket's products, in product order
+      sm.key[i] = (unsigned)(bw.stg_col[D.off + i] - D.blo);
+      sm.pval[i] = sv[D.off + i];
     }
     __syncthreads();
-    unsigned k[kSIPT];
-    unsigned short ix[kSIPT];
-#pragma unroll
-    for (int i = 0; i < kSIPT; ++i) {
-      k[i] = sm.key[tid * kSIPT + i];
-      ix[i] = (unsigned short)(tid * kSIPT + i);
-    }
-    __syncthreads();
-    typename SM::Sort(sm.sort).Sort(k, ix, 0, D.sh > 0 ? D.sh : 1);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kSIPT; ++i) {
-      const int p = tid * kSIPT + i;
-      sm.key[p] = k[i];
-      if (p < n) sm.sval[p] = sm.val[ix[i]];
-    }
-    __syncthreads();
-    // compress: heads of runs of equal columns; sums left to right (lines 9, 11)
-    int heads = 0;
-    V v[kSIPT];
-#pragma unroll
-    for (int i = 0; i < kSIPT; ++i) {
-      const int p = tid * kSIPT + i;
-      const bool head = p < n && (p == 0 || sm.key[p - 1] != k[i]);
-      if (head) {
-        ++heads;
-        V acc = sm.sval[p];
-        for (int x = p + 1; x < n && sm.key[x] == k[i]; ++x) acc = Arith<V>::add(acc, sm.sval[x]);
-        v[i] = acc;
-      } else {
-        k[i] = 0xffffffffu;
-      }
-    }
-    int uniq;
-    int pos = bk_block_excl_scan<kSNT>(heads, &uniq, s_w);  // syncs: the reads above are done
-#pragma unroll
-    for (int i = 0; i < kSIPT; ++i) {
-      if (tid * kSIPT + i < n && k[i] != 0xffffffffu) {
-        bw.stg_col[D.off + pos] = (int)k[i] + D.blo;
-        sv[D.off + pos] = v[i];
-        ++pos;
-      }
-    }
+    // sort by (column, p), runs summed left to right; the distinct entries overwrite the items
+    const int pb = escs::sort_products<kSNT, kBkCap, V>(sm, n, D.sh);
+    const int uniq = escs::compress_write<kSNT, kBkCap, V>(sm, n, pb, D.blo, bw.stg_col + D.off, sv + D.off);
     if (tid == 0) bw.desc[d].uniq = uniq;
     __syncthreads();
   }
@@ -328,7 +270,7 @@ cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t m
   }
   if (max_rows > 0) {
     auto kern = a.f32 ? k_bk_sort<float> : k_bk_sort<double>;
-    const size_t bytes = a.f32 ? sizeof(BkSortSmem<float>) : sizeof(BkSortSmem<double>);
+    const size_t bytes = a.f32 ? sizeof(escs::Smem<kBkCap, float>) : sizeof(escs::Smem<kBkCap, double>);
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) != cudaSuccess)
       return e;
     int per_sm = 1;
