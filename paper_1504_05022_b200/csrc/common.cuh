@@ -66,7 +66,8 @@ constexpr int kBkTarget = 2048;
 constexpr int kBkCap = 4096;
 constexpr int kBkMaxBuckets = 512;
 __host__ __device__ inline bool bk_eligible(int64_t u, int64_t W, int64_t min_w) {
-  return W > min_w && u <= int64_t(kBkTarget) * kBkMaxBuckets;
+  // (windows up to 2^29 columns: the bucket sort's key + product-index composite fits 32 bits)
+  return W > min_w && W <= (int64_t(1) << 29) && u <= int64_t(kBkTarget) * kBkMaxBuckets;
 }
 // buckets: NB = next power of two >= ceil(u / kBkTarget); bucket of column c = (c - lo) >> sh,
 // sh = max(0, ceil(log2 W) - log2 NB); ((W - 1) >> sh) + 1 <= NB buckets are used

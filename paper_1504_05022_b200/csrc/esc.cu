@@ -234,11 +234,12 @@ cudaError_t launch_esc_k(const Stage3Args& a, cudaStream_t s) {
 template <int NT, int CAP, typename IT, typename V>
 __global__ void __launch_bounds__(NT) k_esc_bk(Stage3Args a) {
   constexpr int NW = NT / 32;
+  constexpr int UNR = 4;  // products per lane whose loads are in flight together
   using SM = escs::Smem<CAP, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   __shared__ IT s_bs[NT];
-  __shared__ int s_len[NT], s_pex[NT];
+  __shared__ int s_pex[NT + 1];
   __shared__ V s_av[NT];
   __shared__ int s_w[NW + 1];
   __shared__ unsigned s_max[NW];
@@ -251,7 +252,10 @@ __global__ void __launch_bounds__(NT) k_esc_bk(Stage3Args a) {
     const int row = __ldg(a.perm + a.first + r);
     const int lo = __ldg(a.rlo + row);
     const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
-    // 1. expand (lines 3-6 of Algorithm 1): product p of the row at key/pval[p]
+    // 1. expand (lines 3-6 of Algorithm 1): product p of the row at key/pval[p].  Per batch of
+    //    NT a_ij: the batch's products are cut into NW equal ranges, warp w walks its range 32
+    //    products per step (product -> its a_ij by a forward scan of the batch's offsets), with
+    //    the loads of UNR steps issued before their stores.
     int u = 0;
     unsigned kmax = 0;
     for (int64_t e0 = a0; e0 < a1; e0 += NT) {
@@ -266,20 +270,45 @@ __global__ void __launch_bounds__(NT) k_esc_bk(Stage3Args a) {
       }
       int tot;
       const int ex = escs::block_excl_scan<NT>(len, &tot, s_w);
-      s_len[tid] = len;
-      s_pex[tid] = u + ex;
+      s_pex[tid] = ex;
+      if (tid == NT - 1) s_pex[NT] = tot;
       __syncthreads();
       const int na = (int)((a1 - e0) < NT ? (a1 - e0) : NT);
-      for (int t = w; t < na; t += NW) {
-        const IT bs = s_bs[t];
-        const int lt = s_len[t], pe = s_pex[t];
-        const V at = s_av[t];
-        for (int q = lane; q < lt; q += 32) {
-          const unsigned k = (unsigned)(__ldg(a.B.ci + bs + q) - lo);
-          sm.key[pe + q] = k;
-          kmax = k > kmax ? k : kmax;
-          sm.pval[pe + q] = Arith<V>::mul(at, __ldg(vcast<V>(a.B.val) + bs + q));  // line 6
+      const int pw0 = (int)((int64_t(tot) * w) / NW), pw1 = (int)((int64_t(tot) * (w + 1)) / NW);
+      int p = pw0 + lane;
+      // t: the a_ij of product p (largest t with s_pex[t] <= p), by binary search once
+      int t = 0;
+      {
+        int lo2 = 0, hi2 = na - 1;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2 + 1) >> 1;
+          if (s_pex[mid] <= p) lo2 = mid;
+          else hi2 = mid - 1;
         }
+        t = lo2;
+      }
+      for (; p - lane < pw1; p += 32 * UNR) {
+        unsigned kk[UNR];
+        V vv[UNR];
+        int pp[UNR];
+#pragma unroll
+        for (int x = 0; x < UNR; ++x) {
+          const int q = p + 32 * x;
+          pp[x] = q;
+          if (q < pw1) {
+            while (s_pex[t + 1] <= q) ++t;
+            const IT g = s_bs[t] + (IT)(q - s_pex[t]);
+            kk[x] = (unsigned)(__ldg(a.B.ci + g) - lo);
+            vv[x] = Arith<V>::mul(s_av[t], __ldg(vcast<V>(a.B.val) + g));  // line 6
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < UNR; ++x)
+          if (pp[x] < pw1) {
+            sm.key[u + pp[x]] = kk[x];
+            sm.pval[u + pp[x]] = vv[x];
+            kmax = kk[x] > kmax ? kk[x] : kmax;
+          }
       }
       u += tot;
       __syncthreads();
@@ -324,9 +353,10 @@ cudaError_t launch_bk_t(const Stage3Args& a, cudaStream_t s) {
   return i32 ? launch_bk_k<NT, CAP, int, double>(a, s) : launch_bk_k<NT, CAP, int64_t, double>(a, s);
 }
 
-bool esc_old() {
+// the bucket ESC needs key + product-index bits within 32: windows up to 2^29 columns
+bool esc_old(const Stage3Args& a) {
   static const bool v = getenv("SPGEMM_ESC_OLD") != nullptr;  // A/B switch (development)
-  return v;
+  return v || a.n > (int64_t(1) << escs::max_key_bits<8192>());
 }
 
 // ----------------------------------------------------------------------------------------
@@ -538,7 +568,7 @@ cudaError_t launch_merge_t(const Stage3Args& a, cudaStream_t s) {
 // merge (measured faster than the radix sort at these sizes; slower at 4096+, c3a / c5).
 cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  if (!esc_old()) switch (S) {
+  if (!esc_old(a)) switch (S) {
     case 64: return launch_bk_t<32, 64>(a, s);
     case 128: return launch_bk_t<32, 128>(a, s);
     case 256: return launch_bk_t<64, 256>(a, s);
@@ -561,7 +591,7 @@ cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
 // e2048: run merge (5.9 vs 6.3 ms on c3a); e4096 / e8192: radix (merge 25.0 vs 21.1 ms)
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  if (!esc_old()) switch (tier) {
+  if (!esc_old(a)) switch (tier) {
     case T_E2048: return launch_bk_t<256, 2048>(a, s);
     case T_E4096: return launch_bk_t<256, 4096>(a, s);
     case T_E8192: return launch_bk_t<512, 8192>(a, s);

@@ -20,9 +20,11 @@ namespace escs {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// NBMAX buckets at most: enough for ~32 products per bucket, and for key + product bits within
+// 32 while the window has at most kMaxKeyBits(CAP) bits (launchers check n against it)
 template <int CAP, typename V>
 struct Smem {
-  static constexpr int NBMAX = CAP / 2;
+  static constexpr int NBMAX = CAP / 8;
   unsigned key[CAP];
   V pval[CAP];
   unsigned arr[CAP];
@@ -31,6 +33,11 @@ struct Smem {
 };
 
 __device__ __forceinline__ int ceil_log2(unsigned x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); }
+// widest key (window) the composite (key low bits, p) fits 32 bits for with NBMAX buckets
+template <int CAP>
+__host__ __device__ constexpr int max_key_bits() { return 32 - ilog2c(CAP) + ilog2c(CAP / 8); }
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* total, int* s_w) {
