@@ -50,6 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
              "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", inc]
     if os.environ.get("SPGEMM_PTXAS_V"):
         flags += ["-Xptxas", "-v"]
+    if os.environ.get("SPGEMM_DEFS"):  # development A/B builds: extra -D definitions
+        flags += ["-D" + d for d in os.environ["SPGEMM_DEFS"].split()]
 
     def one(src):
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
