@@ -119,6 +119,7 @@ struct spgemm_handle_s {
   int64_t* pinned = nullptr;  // host pinned scratch [kSumLen + 8]
   // long rows
   int64_t nlong = 0, long_first = 0;
+  const int32_t* long_perm = nullptr;  // progressive long rows are long_perm[long_first, +nlong)
   LongState* lst = nullptr;
   int32_t* lact = nullptr;       // active long rows of a round
   int32_t* lovf = nullptr;       // rows that checkpointed (overflowed) in a round
@@ -208,6 +209,7 @@ void free_symbolic(spgemm_handle_t h) {
   h->lst = nullptr;
   h->lact = h->lovf = h->lovf_cnt = nullptr;
   h->lsizes = h->loff = h->ltable = nullptr;
+  h->long_perm = nullptr;
   if (h->arena_col.base || h->arena_val.base) {
     cudaStreamSynchronize(h->stream);  // unmapping is immediate, not stream-ordered
     vmm_release(&h->arena_col);
@@ -268,6 +270,53 @@ spgemm_status_t long_grow_arena(spgemm_handle_t h, const int32_t* list, int64_t 
   return SPGEMM_SUCCESS;
 }
 
+// Long rows with wide windows on the bucket path (longbk.cu), output rows at out_off (C: precise
+// numeric; C~ slices: hybrid symbolic).  Staging and bucket tables live for this call only
+// (stream-ordered pool).  Rows the path does not take are listed in fb (its count goes to
+// pinned[1] as int32, for the hybrid's progressive path) or, with rank_fallback, computed by
+// the rank kernel right away (precise).
+spgemm_status_t run_long_buckets(spgemm_handle_t h, const int64_t* out_off, int32_t* out_col, double* out_val,
+                                 int64_t* nnz_row, int32_t* fb, bool rank_fallback) {
+  Stage3Args a{};
+  a.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
+  a.A = h->A;
+  a.B = h->B;
+  a.b_nnz = h->b_nnz;
+  a.n = h->n;
+  a.perm = h->ws.perm;
+  a.first = h->long_first;
+  a.count = h->nlong;
+  a.out_off = out_off;
+  a.out_col = out_col;
+  a.out_val = out_val;
+  a.nnz_row = nnz_row;
+  a.mode = MODE_FILL;
+  a.bwin = h->ws.bwin;
+  a.rlo = h->ws.rlo;
+  a.rhi = h->ws.rhi;
+  a.U = h->ws.U;
+  if (!h->work_ctr) AL(h, &h->work_ctr, 1);
+  a.work_ctr = h->work_ctr;
+  const int64_t ndesc = h->bk_u / 1024 + h->bk_rows;
+  const size_t vb = vbytes(h);
+  const size_t sz[7] = {sizeof(int32_t) * size_t(h->bk_u), vb * size_t(h->bk_u), sizeof(BkDesc) * size_t(ndesc),
+                        sizeof(BkRow) * size_t(h->bk_rows), 2 * sizeof(unsigned long long), 2 * sizeof(int32_t),
+                        sizeof(int32_t) * size_t(h->nlong)};
+  void* p[7] = {};
+  for (int q = 0; q < 7; ++q)
+    if (q != 6 || !fb) CK(h, pool_malloc(&p[q], sz[q], h->stream));
+  BkWork bw{static_cast<int32_t*>(p[0]), static_cast<double*>(p[1]), static_cast<BkDesc*>(p[2]),
+            static_cast<BkRow*>(p[3]), static_cast<unsigned long long*>(p[4]), static_cast<int32_t*>(p[5]),
+            fb ? fb : static_cast<int32_t*>(p[6]), h->bk_min_w};
+  cudaError_t e = launch_long_buckets(a, bw, h->bk_rows, rank_fallback, h->stream);
+  if (e == cudaSuccess && !rank_fallback)
+    e = cudaMemcpyAsync(h->pinned + 1, bw.cur32 + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
+  for (int q = 0; q < 7; ++q)
+    if (p[q]) cudaFreeAsync(p[q], h->stream);
+  CK(h, e);
+  return SPGEMM_SUCCESS;
+}
+
 // Long rows of the hybrid strategy: the paper's group 5 with progressive allocation
 // ([P:297]).  Every long row starts with C0 entries (16 Ki; SPGEMM_FLAG_UPPER_BOUND: min(u_i,
 // n)) in the long-row arena and runs the bitmap rank kernel tile by tile; a tile that does not
@@ -299,7 +348,7 @@ spgemm_status_t run_long(spgemm_handle_t h) {
   CK(h, vmm_reserve(&h->arena_col, totalb / 2));
   CK(h, vmm_reserve(&h->arena_val, totalb));
   h->long_entries = 0;
-  CK(h, launch_long_init(h->lst, h->ws.perm, h->long_first, nl, h->ws.U, h->n, cap0, h->lsizes, h->stream));
+  CK(h, launch_long_init(h->lst, h->long_perm, h->long_first, nl, h->ws.U, h->n, cap0, h->lsizes, h->stream));
   spgemm_status_t s = long_grow_arena(h, nullptr, nl);
   if (s != SPGEMM_SUCCESS) return s;
   const unsigned g = (unsigned)((nl + 255) / 256);
@@ -313,7 +362,7 @@ spgemm_status_t run_long(spgemm_handle_t h) {
     a.B = h->B;
     a.b_nnz = h->b_nnz;
     a.n = h->n;
-    a.perm = h->ws.perm;
+    a.perm = h->long_perm;
     a.first = h->long_first;
     a.count = nactive;
     a.nnz_row = h->nnz_row;
@@ -531,7 +580,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   // column sets of the window-bitmap rows (4 B/entry) for its numeric pass
   const int cap_mode = precise ? CAP_PRECISE : CAP_HYBRID;
   CK(h, launch_stage1(m, h->k, h->n, h->A, h->B, tp, cap_mode, ws, h->stream));
-  CK(h, launch_stage2(m, ws, cap_mode, h->n, h->stream));
+  CK(h, launch_stage2(m, ws, cap_mode, h->n, tp.bk_min_w, h->stream));
   h->launches_sym = 3;
   tr("alloc + stage 1-2");
   CK(h, cudaMemcpyAsync(h->pinned, ws.summary, sizeof(int64_t) * kSumLen, cudaMemcpyDeviceToHost, h->stream));
@@ -548,6 +597,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->max_u = h->pinned[kSumUMax];
   h->bw_wmax = h->pinned[kSumWmax];
   h->bw_vmax = h->pinned[kSumVmax];
+  h->bk_u = h->pinned[kSumBkU];  // hybrid: long rows on the bucket path (precise: after re-binning)
+  h->bk_rows = h->pinned[kSumBkRows];
   // precise: C~ holds only the window-bitmap rows' sorted column sets (STRUCT); sum_cap counts
   // only those rows (ctil_capacity, CAP_PRECISE)
   AL(h, &h->ctil_col, h->sum_cap > 0 ? h->sum_cap : 1);
@@ -589,7 +640,22 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   tr("stage 3 classes");
   h->nlong = h->tier_count[T_LONG];
   h->long_first = h->tier_off[T_LONG];
+  h->long_perm = ws.perm;
   if (h->nlong > 0) cudaEventRecord(h->tsym[T_LONG][0], h->stream);
+  if (hybrid && h->nlong > 0 && h->bk_rows > 0) {
+    // long rows with wide windows: bucket path into their C~ slices (upper-bound capacity);
+    // the others continue on the progressive path below, listed in long_perm
+    int32_t* fb = nullptr;
+    AL(h, &fb, h->nlong);
+    s = run_long_buckets(h, h->ws.ctil_off, h->ctil_col, h->ctil_val, h->nnz_row, fb, false);
+    if (s != SPGEMM_SUCCESS) return s;
+    h->launches_sym += 4;
+    s = sync(h);
+    if (s != SPGEMM_SUCCESS) return s;
+    h->long_perm = fb;
+    h->long_first = 0;
+    h->nlong = *reinterpret_cast<int32_t*>(h->pinned + 1);
+  }
   if (hybrid) {
     // the paper's group 5: progressive allocation with checkpoint / 2x growth [P:297]; the
     // rows' sorted results (values in the oracle's order) are their C~ slices in the long-row
@@ -680,11 +746,12 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
     CopyArgs ca{};
     ca.f32 = (h->flags & SPGEMM_FLAG_FP32) != 0;
     ca.m = h->m;
-    ca.perm = h->ws.perm;
+    ca.perm = h->long_perm;
     ca.long_first = h->long_first;
     ca.nlong = h->nlong;
     ca.c_rp = h->c_rp;
     ca.ctil_off = h->ws.ctil_off;
+    ca.ctil_total = h->sum_cap;
     ca.tier = h->ws.tier;
     ca.ctil_col = h->ctil_col;
     ca.ctil_val = h->ctil_val;
@@ -747,21 +814,9 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
         a.work_ctr = h->work_ctr;
         cudaEventRecord(h->tev[T_LONG][0], h->stream);
         if (h->bk_rows > 0) {
-          // wide windows: bucket partition + per-bucket sort (longbk.cu); the rest: rank kernel.
-          // Workspace for this call only (stream-ordered pool, freed after the launches).
-          const int64_t ndesc = h->bk_u / 1024 + h->bk_rows;
-          const size_t vb = vbytes(h);
-          const size_t sz[7] = {sizeof(int32_t) * size_t(h->bk_u), vb * size_t(h->bk_u), sizeof(BkDesc) * size_t(ndesc),
-                                sizeof(BkRow) * size_t(h->bk_rows), 2 * sizeof(unsigned long long),
-                                2 * sizeof(int32_t), sizeof(int32_t) * size_t(h->nlong)};
-          void* p[7] = {};
-          for (int q = 0; q < 7; ++q) CK(h, pool_malloc(&p[q], sz[q], h->stream));
-          BkWork bw{static_cast<int32_t*>(p[0]), static_cast<double*>(p[1]), static_cast<BkDesc*>(p[2]),
-                    static_cast<BkRow*>(p[3]), static_cast<unsigned long long*>(p[4]), static_cast<int32_t*>(p[5]),
-                    static_cast<int32_t*>(p[6]), h->bk_min_w};
-          const cudaError_t e = launch_long_buckets(a, bw, h->bk_rows, h->stream);
-          for (int q = 0; q < 7; ++q) cudaFreeAsync(p[q], h->stream);
-          CK(h, e);
+          // wide windows: bucket partition + per-bucket sort (longbk.cu); the rest: rank kernel
+          spgemm_status_t s2 = run_long_buckets(h, h->c_rp, c_col_idx, c_val, nullptr, nullptr, true);
+          if (s2 != SPGEMM_SUCCESS) return s2;
           h->launches_num += 4;
         } else {
           CK(h, launch_long_bitmap(a, h->stream));

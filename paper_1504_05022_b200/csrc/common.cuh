@@ -165,17 +165,19 @@ __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_cl
 }
 
 // Hybrid C~ capacity of a row ([P:224]: u_i for short rows; here min(u_i, n) which is
-// still a safe bound since nnz(c_i*) <= n).  Long rows live in their own growing arena.
-__host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n) {
-  if (t == T_LONG) return 0;
+// still a safe bound since nnz(c_i*) <= n).  Long rows live in their own growing arena —
+// except long rows with wide windows (bk_eligible), which take the bucket path (longbk.cu)
+// into a C~ slice of the upper bound (these rows' products rarely repeat a column).
+__host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n, int64_t W, int64_t bk_min_w) {
+  if (t == T_LONG && !bk_eligible(u, W, bk_min_w)) return 0;
   return u < n ? u : n;
 }
 // C~ capacity by strategy: CAP_HYBRID keeps whole rows (columns + values) in C~; CAP_PRECISE
 // keeps only the sorted column sets of the window-bitmap rows (STRUCT -> DENSE), no other row
 // needs C~ in the precise strategy.
 enum CapMode : int { CAP_NONE = 0, CAP_HYBRID = 1, CAP_PRECISE = 2 };
-__host__ __device__ inline int64_t ctil_capacity(int mode, int t, int64_t u, int64_t n) {
-  if (mode == CAP_HYBRID) return hybrid_capacity(t, u, n);
+__host__ __device__ inline int64_t ctil_capacity(int mode, int t, int64_t u, int64_t n, int64_t W, int64_t bk_min_w) {
+  if (mode == CAP_HYBRID) return hybrid_capacity(t, u, n, W, bk_min_w);
   if (mode == CAP_PRECISE && t == T_BW) return u < n ? u : n;
   return 0;
 }
@@ -289,7 +291,7 @@ constexpr int kSumLen = kSumU + 8;
 
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           int cap_mode, Stage12Ws& ws, cudaStream_t s);
-cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, cudaStream_t s);
+cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, int64_t bk_min_w, cudaStream_t s);
 // PRECISE: re-bin rows by (u_i, nnz(c_i*)) into ws.tier/perm (ws.U and nnz_row are inputs).
 cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParams tp, Stage12Ws& ws,
                          cudaStream_t s);
@@ -328,7 +330,9 @@ struct BkWork {
   int32_t* fb_list;          // those rows
   int64_t min_w;             // bk_eligible window threshold
 };
-cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t max_rows, cudaStream_t s);
+// rank_fallback: run the rank kernel on the rows left over (precise); else only list them
+cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t max_rows, bool rank_fallback,
+                                cudaStream_t s);
 
 // Exclusive scan of int64 values x[0..len) into y[0..len]; y[len] = total.  tmp must hold
 // scan_tmp_elems(len) int64.
@@ -389,7 +393,8 @@ struct CopyArgs {
   const int32_t* perm;       // long rows are perm[long_first, long_first + nlong)
   int64_t long_first, nlong;
   const int64_t* c_rp;       // final row pointers [m+1]
-  const int64_t* ctil_off;   // by row (C~ offsets; unused for long rows)
+  const int64_t* ctil_off;   // by row (C~ offsets; rows with an empty slice live in the arena)
+  int64_t ctil_total;        // C~ entries (the end of the last row's slice)
   const uint8_t* tier;
   const int32_t* ctil_col;
   const double* ctil_val;

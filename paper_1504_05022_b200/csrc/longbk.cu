@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kSNT) k_bk_sort(BkWork bw) {
 // ------------------------------------------------------------------------------- copy to C
 template <typename V>
 __global__ void __launch_bounds__(kCNT) k_bk_copy(BkWork bw, const int64_t* __restrict__ c_rp,
-                                                  int32_t* __restrict__ out_col, double* out_val) {
+                                                  int32_t* __restrict__ out_col, double* out_val,
+                                                  int64_t* __restrict__ nnz_row) {
   __shared__ int s_off[kBkMaxBuckets + 1];
   __shared__ int s_w[kCNT / 32 + 1];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(kCNT) k_bk_copy(BkWork bw, const int64_t* __re
     }
     int tot;
     const int ex = bk_block_excl_scan<kCNT>(x[0] + x[1], &tot, s_w);
+    if (tid == 0 && nnz_row) nnz_row[R.row] = tot;  // hybrid: the row's length
     if (2 * tid < R.nbk) s_off[2 * tid] = ex;
     if (2 * tid + 1 < R.nbk) s_off[2 * tid + 1] = ex + x[0];
     __syncthreads();
@@ -250,7 +252,8 @@ __global__ void __launch_bounds__(kCNT) k_bk_copy(BkWork bw, const int64_t* __re
 
 }  // namespace
 
-cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t max_rows, cudaStream_t s) {
+cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t max_rows, bool rank_fallback,
+                                cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const int sms = num_sms();
   cudaError_t e = cudaMemsetAsync(bw.cur64, 0, 2 * sizeof(unsigned long long), s);
@@ -279,9 +282,10 @@ cudaError_t launch_long_buckets(const Stage3Args& a, const BkWork& bw, int64_t m
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     auto kc = a.f32 ? k_bk_copy<float> : k_bk_copy<double>;
     const int64_t g = max_rows < int64_t(sms) * 8 ? max_rows : int64_t(sms) * 8;
-    kc<<<(unsigned)g, kCNT, 0, s>>>(bw, a.out_off, a.out_col, a.out_val);
+    kc<<<(unsigned)g, kCNT, 0, s>>>(bw, a.out_off, a.out_col, a.out_val, a.nnz_row);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  if (!rank_fallback) return cudaSuccess;
   // rows that stay on the rank kernel
   Stage3Args b = a;
   b.perm = bw.fb_list;

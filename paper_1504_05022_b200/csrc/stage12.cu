@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * NT * RPT;
   int64_t capsum = 0, usum = 0, umax = 0, wmax = 0, vmax = 0;
+  unsigned long long bku = 0, bkr = 0;
 #pragma unroll 1
   for (int r = 0; r < RPT; ++r) {
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
@@ -116,7 +117,11 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
       rlo[i] = lo;
       rhi[i] = hi;
       atomicAdd(&s_hist[t], 1);
-      capsum += ctil_capacity(cap_mode, t, u, n);
+      capsum += ctil_capacity(cap_mode, t, u, n, W, tp.bk_min_w);
+      if (cap_mode == CAP_HYBRID && t == T_LONG && bk_eligible(u, W, tp.bk_min_w)) {
+        bku += (unsigned long long)u;  // hybrid long rows on the bucket path
+        ++bkr;
+      }
       usum += u;
       umax = u > umax ? u : umax;
       if (t == T_BW) {
@@ -125,6 +130,15 @@ __global__ void __launch_bounds__(NT) k_stage1(int64_t m, int64_t n, CsrView A,
         vmax = v > vmax ? v : vmax;
       }
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bku += __shfl_xor_sync(0xffffffffu, bku, o);
+    bkr += __shfl_xor_sync(0xffffffffu, bkr, o);
+  }
+  if ((threadIdx.x & 31) == 0 && bkr > 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(summary + kSumBkU), bku);
+    atomicAdd(reinterpret_cast<unsigned long long*>(summary + kSumBkRows), bkr);
   }
   // window maxima of the bw rows: one global atomic per block (the same two addresses for
   // every block: per-row or per-warp atomics serialise at L2)
@@ -293,9 +307,11 @@ __global__ void __launch_bounds__(NT) k_stage2_scan(int64_t nblk, int32_t* blk_t
 }
 
 template <int NT, int RPT>
-__global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int cap_mode,
+__global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int cap_mode, int64_t bk_min_w,
                                                        const uint8_t* __restrict__ tier,
                                                        const int64_t* __restrict__ U,
+                                                       const int32_t* __restrict__ rlo,
+                                                       const int32_t* __restrict__ rhi,
                                                        const int32_t* __restrict__ blk_tier_off,
                                                        const int64_t* __restrict__ blk_cap_off,
                                                        int32_t* __restrict__ perm,
@@ -315,7 +331,8 @@ __global__ void __launch_bounds__(NT) k_stage2_scatter(int64_t m, int64_t n, int
     const int64_t i = base + int64_t(r) * NT + threadIdx.x;
     const bool valid = i < m;
     const int t = valid ? (int)tier[i] : NUM_TIERS;
-    const int64_t cap = valid ? ctil_capacity(cap_mode, t, U[i], n) : 0;
+    const int64_t cap = valid && cap_mode != CAP_NONE
+                            ? ctil_capacity(cap_mode, t, U[i], n, int64_t(rhi[i]) - rlo[i] + 1, bk_min_w) : 0;
     const unsigned peers = __match_any_sync(0xffffffffu, t);
     const int wrank = __popc(peers & lanemask_lt());
     if (wrank == 0) s_wcnt[w][t] = __popc(peers);
@@ -439,7 +456,7 @@ __global__ void k_validate(int64_t rows, int64_t cols, const int64_t* __restrict
 cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B, TierParams tp,
                           int cap_mode, Stage12Ws& ws, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 3 * sizeof(int64_t), s);
+  cudaError_t e = cudaMemsetAsync(ws.summary + kSumWmax, 0, 5 * sizeof(int64_t), s);  // .. kSumBkRows
   if (e != cudaSuccess) return e;
   if (k > 0) k_bwin<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, B.rp, B.ci, ws.bwin);
   k_stage1<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
@@ -448,13 +465,13 @@ cudaError_t launch_stage1(int64_t m, int64_t k, int64_t n, CsrView A, CsrView B,
   return cudaGetLastError();
 }
 
-cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, cudaStream_t s) {
+cudaError_t launch_stage2(int64_t m, Stage12Ws& ws, int cap_mode, int64_t n, int64_t bk_min_w, cudaStream_t s) {
   k_stage2_scan<1024><<<1, 1024, 0, s>>>(ws.nblk, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax,
                                          ws.summary);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || m == 0) return e;
   k_stage2_scatter<kS12Threads, kS12RowsPerThread><<<(unsigned)ws.nblk, kS12Threads, 0, s>>>(
-      m, n, cap_mode, ws.tier, ws.U, ws.blk_tier, ws.blk_cap, ws.perm, ws.ctil_off);
+      m, n, cap_mode, bk_min_w, ws.tier, ws.U, ws.rlo, ws.rhi, ws.blk_tier, ws.blk_cap, ws.perm, ws.ctil_off);
   return cudaGetLastError();
 }
 
@@ -469,7 +486,7 @@ cudaError_t launch_rebin(int64_t m, int64_t n, const int64_t* nnz_row, TierParam
       m, n, ws.U, nnz_row, tp, ws.rlo, ws.rhi, ws.tier, ws.blk_tier, ws.blk_cap, ws.blk_usum, ws.blk_umax, ws.summary);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_stage2(m, ws, CAP_NONE, n, s);
+  return launch_stage2(m, ws, CAP_NONE, n, tp.bk_min_w, s);
 }
 
 int64_t scan_tmp_elems(int64_t len) { return (len + kScanTile - 1) / kScanTile + 2; }

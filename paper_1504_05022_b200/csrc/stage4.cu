@@ -25,7 +25,10 @@ __global__ void __launch_bounds__(256) k_copy_flat(CopyArgs a) {
     const int64_t end = __shfl_sync(0xffffffffu, has ? __ldg(a.c_rp + i + 1) : rp, 31);
     const int64_t beg = __shfl_sync(0xffffffffu, rp, 0);
     const int64_t src = has ? __ldg(a.ctil_off + i) : 0;
-    const bool lng = has && a.tier[i] == T_LONG;
+    // long rows without a C~ slice live in the arena (progressive path); long rows of the
+    // bucket path have an upper-bound slice like every other class
+    const bool lng = has && a.tier[i] == T_LONG &&
+                     (i + 1 < a.m ? __ldg(a.ctil_off + i + 1) : a.ctil_total) == src;
     for (int64_t p0 = beg; p0 < end; p0 += 32) {
       const int64_t p = p0 + lane;
       // last lane k with rp_k <= p (rows are ascending; empty rows share rp values)
