@@ -641,7 +641,8 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   h->nlong = h->tier_count[T_LONG];
   h->long_first = h->tier_off[T_LONG];
   h->long_perm = ws.perm;
-  if (h->nlong > 0) cudaEventRecord(h->tsym[T_LONG][0], h->stream);
+  const bool any_long = h->nlong > 0;
+  if (any_long) cudaEventRecord(h->tsym[T_LONG][0], h->stream);
   if (hybrid && h->nlong > 0 && h->bk_rows > 0) {
     // long rows with wide windows: bucket path into their C~ slices (upper-bound capacity);
     // the others continue on the progressive path below, listed in long_perm
@@ -682,7 +683,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     CK(h, launch_long_bitmap(a, h->stream));
     h->launches_sym += 1;
   }
-  if (h->nlong > 0) {
+  if (any_long) {
     cudaEventRecord(h->tsym[T_LONG][1], h->stream);
     h->tsym_used[T_LONG] = true;
   }
