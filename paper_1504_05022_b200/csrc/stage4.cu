@@ -29,23 +29,40 @@ __global__ void __launch_bounds__(256) k_copy_flat(CopyArgs a) {
     // bucket path have an upper-bound slice like every other class
     const bool lng = has && a.tier[i] == T_LONG &&
                      (i + 1 < a.m ? __ldg(a.ctil_off + i + 1) : a.ctil_total) == src;
-    for (int64_t p0 = beg; p0 < end; p0 += 32) {
-      const int64_t p = p0 + lane;
-      // last lane k with rp_k <= p (rows are ascending; empty rows share rp values)
-      int lo = 0;
+    // four 32-entry chunks per iteration: their loads are in flight together
+    constexpr int U = 4;
+    for (int64_t p0 = beg; p0 < end; p0 += 32 * U) {
+      int64_t q[U];
 #pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int64_t v = __shfl_sync(0xffffffffu, rp, lo + step);
-        if (lo + step < 32 && v <= p) lo += step;
+      for (int x = 0; x < U; ++x) {
+        const int64_t p = p0 + 32 * x + lane;
+        // last lane k with rp_k <= p (rows are ascending; empty rows share rp values)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int64_t v = __shfl_sync(0xffffffffu, rp, lo + step);
+          if (lo + step < 32 && v <= p) lo += step;
+        }
+        const int64_t rbeg = __shfl_sync(0xffffffffu, rp, lo);
+        const int64_t rsrc = __shfl_sync(0xffffffffu, src, lo);
+        const bool rl = __shfl_sync(0xffffffffu, lng, lo);
+        q[x] = (p < end && !rl) ? rsrc + (p - rbeg) : -1;
       }
-      const int64_t rbeg = __shfl_sync(0xffffffffu, rp, lo);
-      const int64_t rsrc = __shfl_sync(0xffffffffu, src, lo);
-      const bool rl = __shfl_sync(0xffffffffu, lng, lo);
-      if (p < end && !rl) {
-        const int64_t q = rsrc + (p - rbeg);
-        a.c_col[p] = __ldcs(a.ctil_col + q);
-        vcast<V>(a.c_val)[p] = __ldcs(vcast<V>(a.ctil_val) + q);
-      }
+      int cv[U];
+      V vv[U];
+#pragma unroll
+      for (int x = 0; x < U; ++x)
+        if (q[x] >= 0) {
+          cv[x] = __ldcs(a.ctil_col + q[x]);
+          vv[x] = __ldcs(vcast<V>(a.ctil_val) + q[x]);
+        }
+#pragma unroll
+      for (int x = 0; x < U; ++x)
+        if (q[x] >= 0) {
+          const int64_t p = p0 + 32 * x + lane;
+          a.c_col[p] = cv[x];
+          vcast<V>(a.c_val)[p] = vv[x];
+        }
     }
   }
 }
