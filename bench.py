@@ -498,7 +498,9 @@ def run_gpu(args):
     if world == 1 and not args.no_per_config:
         per = {}
         for cfg in PER_CONFIG:
-            for strat in (["precise", "hybrid"] if cfg == "c2" else ["precise"]):
+            # both strategies where they trade places: c2 (precise ahead: r_c = 5.8, C~ 6x C),
+            # c3a / c3b (power law: hybrid saves the counting pass where r_c is near 1)
+            for strat in (["precise", "hybrid"] if cfg in ("c2", "c3a", "c3b") else ["precise"]):
                 if cfg == args.config and strat == args.strategy:
                     continue
                 torch.cuda.empty_cache()

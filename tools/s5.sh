@@ -19,7 +19,7 @@ print(' '.join(seen))"); do
   python tools/profile_report.py $OUT/$1.md $OUT/$1.ncu-rep > /dev/null 2>&1
   [ -n "$KEEP" ] || rm -f $OUT/$1.ncu-rep
 }
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"${KRE:-k_esc_merge|k_esc_sort|k_bk_|k_wrow|k_cta_hash|k_long}" -c ${NC3A:-24} -o $OUT/c3a python bench.py --config ${CFG1:-c3a} --steps 1 --warmup 1 --no-e2e --no-cpu --no-per-config > $OUT/ncu_c3a.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base ${KBASE:-function} -k regex:"${KRE:-k_esc_merge|k_esc_sort|k_bk_|k_wrow|k_cta_hash|k_long}" -c ${NC3A:-24} -o $OUT/c3a python bench.py --config ${CFG1:-c3a} --steps 1 --warmup 1 --no-e2e --no-cpu --no-per-config > $OUT/ncu_c3a.log 2>&1
 summ c3a
 if [ -z "$SKIP2" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_long" -c 2 -o $OUT/c3b python bench.py --config c3b --steps 1 --warmup 1 --no-e2e --no-cpu --no-per-config > $OUT/ncu_c3b.log 2>&1
