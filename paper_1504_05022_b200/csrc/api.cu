@@ -42,6 +42,17 @@ __global__ void k_tier_to_i32(const uint8_t* t, int32_t* o, int64_t m) {
   if (i < m) o[i] = t[i];
 }
 
+// max of nnz_row over the rows perm[first, first + count) (the window class's exact row length)
+__global__ void k_rows_max(const int32_t* __restrict__ perm, int64_t first, int64_t count,
+                           const int64_t* __restrict__ nnz_row, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < count; r += int64_t(gridDim.x) * blockDim.x)
+    m = max(m, (unsigned long long)nnz_row[perm[first + r]]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+}
+
 __global__ void k_iota(int32_t* p, int64_t n) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = (int32_t)i;
@@ -572,7 +583,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
   // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
   CK(h, cudaMemsetAsync(h->nnz_row, 0, sizeof(int64_t) * m, h->stream));
-  TierParams tp{g_force_tier, g_long_threshold, g_bk_min_w};
+  TierParams tp{g_force_tier, g_long_threshold, g_bk_min_w, precise ? 1 : 0};
   h->bk_min_w = g_bk_min_w;
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = h->tsym_used[t] = false;
@@ -632,7 +643,31 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
       AL(h, &a.bw_ovf_cnt, 1);
     }
     cudaEventRecord(h->tsym[t][0], h->stream);
-    CK(h, launch_stage3_tier(t, a, h->stream));
+    if (hybrid && t == T_BW) {
+      // window rows in the hybrid strategy: the structure pass (sorted column sets into the
+      // rows' C~ slices), the exact row-length maximum, then the values by rank (DENSE) into
+      // the same slices — the precise strategy's two walks, with C~ as their output
+      a.mode = MODE_STRUCT;
+      CK(h, launch_stage3_tier(t, a, h->stream));
+      CK(h, cudaMemsetAsync(ws.summary + kSumVmax, 0, sizeof(int64_t), h->stream));
+      k_rows_max<<<256, 256, 0, h->stream>>>(ws.perm, a.first, a.count, h->nnz_row,
+                                              reinterpret_cast<unsigned long long*>(ws.summary + kSumVmax));
+      CK(h, cudaGetLastError());
+      CK(h, cudaMemcpyAsync(h->pinned + kSumVmax, ws.summary + kSumVmax, 2 * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, h->stream));  // kSumVmax, kSumBmax
+      s = sync(h);
+      if (s != SPGEMM_SUCCESS) return s;
+      a.mode = MODE_DENSE;
+      a.struct_col = h->ctil_col;
+      a.struct_off = ws.ctil_off;
+      a.nnz_row = nullptr;
+      a.bw_vmax = h->pinned[kSumVmax];
+      a.bw_bmax = h->pinned[kSumBmax];
+      CK(h, launch_stage3_tier(t, a, h->stream));
+      h->launches_sym += 2;
+    } else {
+      CK(h, launch_stage3_tier(t, a, h->stream));
+    }
     cudaEventRecord(h->tsym[t][1], h->stream);
     h->tsym_used[t] = true;
     ++h->launches_sym;

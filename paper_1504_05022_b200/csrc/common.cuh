@@ -45,15 +45,20 @@ constexpr int kEmptyKey = -1;
 // Window-bitmap class limits: column window W (bits per warp) and row length (values per warp).
 constexpr int64_t kBwMaxW = int64_t(1) << 17;
 constexpr int64_t kBwMaxV = 2048;
+// precise strategy: the bound may reach kBwMaxVRelax — the exact length decides at re-binning
+// (rows longer than kBwMaxV leave the class), so rows whose products repeat columns many times
+// (Galerkin products: u of 3-8 Ki, nnz of a few hundred) keep the dense accumulator
+constexpr int64_t kBwMaxVRelax = 8192;
 
-__host__ __device__ inline bool bw_ok(int64_t cap, int64_t W) {
-  return W > 0 && W <= kBwMaxW && (cap < W ? cap : W) <= kBwMaxV;
+__host__ __device__ inline bool bw_ok(int64_t cap, int64_t W, int64_t vmax = kBwMaxV) {
+  return W > 0 && W <= kBwMaxW && (cap < W ? cap : W) <= vmax;
 }
 
 struct TierParams {
   int force_tier;         // -1 = off
   int64_t long_threshold; // rows with cap above go long (0 = default by smem)
   int64_t bk_min_w;       // precise long rows: window above which values take the bucket path
+  int bw_relax;           // precise: window rows by the relaxed bound (kBwMaxVRelax)
 };
 
 // Long rows, precise numeric: rows whose column window is wider than one bitmap tile of the
@@ -111,7 +116,7 @@ __host__ __device__ inline int classify(int64_t u, int64_t n, TierParams p, int6
     while ((int64_t(1) << g) < u) ++g;
     return T_G1 + g;
   }
-  if (bw_ok(cap, W)) return T_BW;
+  if (bw_ok(cap, W, p.bw_relax ? kBwMaxVRelax : kBwMaxV)) return T_BW;
   for (int t = T_W64; t <= T_W2048; ++t)
     if (tier_capacity_ok(t, u, cap, W)) return t;
   const int e = esc_class(u);  // products fit one CTA's shared memory: bucket ESC
@@ -137,7 +142,7 @@ __host__ __device__ inline int tier_exact_ok(int t, int64_t u, int64_t nnz) {
 // that only the symbolic warp classes (STRUCT) produce.
 __host__ __device__ inline int classify_exact(int64_t u, int64_t nnz, int sym_class, TierParams p) {
   if (u == 0) return T_EMPTY;
-  if (sym_class == T_BW) return T_BW;  // window and bound unchanged: nnz <= min(u, W) <= kBwMaxV
+  if (sym_class == T_BW && nnz <= kBwMaxV) return T_BW;  // longer rows (relaxed bound): ESC / CTA classes
   // warp classes: the numeric pass sorts the row's u <= 0.8·S products in one CTA (ESC)
   if (p.force_tier < 0 && sym_class >= T_W64 && sym_class <= T_W2048) return sym_class;
   // long rows stay on the bitmap path (ranks, no sort): c3b rows with u > 8192 but

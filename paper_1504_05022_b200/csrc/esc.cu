@@ -574,7 +574,10 @@ cudaError_t launch_esc_items(int S, const Stage3Args& a, cudaStream_t s) {
     case 256: return launch_bk_t<64, 256>(a, s);
     case 512: return launch_bk_t<64, 512>(a, s);
     case 1024: return launch_bk_t<128, 1024>(a, s);
-    case 2048: return launch_bk_t<256, 2048>(a, s);
+#ifndef SG_W2048_NT
+#define SG_W2048_NT 256
+#endif
+    case 2048: return launch_bk_t<SG_W2048_NT, 2048>(a, s);
     default: return cudaErrorInvalidValue;
   }
   switch (S) {
@@ -593,7 +596,10 @@ cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   if (!esc_old(a)) switch (tier) {
     case T_E2048: return launch_bk_t<256, 2048>(a, s);
-    case T_E4096: return launch_bk_t<256, 4096>(a, s);
+#ifndef SG_E4096_NT
+#define SG_E4096_NT 256
+#endif
+    case T_E4096: return launch_bk_t<SG_E4096_NT, 4096>(a, s);
     case T_E8192: return launch_bk_t<512, 8192>(a, s);
     default: return cudaErrorInvalidValue;
   }

@@ -137,7 +137,10 @@ __device__ __forceinline__ int sort_products(Smem<CAP, V>& sm, int u, int kb) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int pb = ceil_log2((unsigned)u) > 0 ? ceil_log2((unsigned)u) : 1;
-  int lnb = ceil_log2((unsigned)((u + 31) / 32));
+#ifndef SG_ESC_BKT
+#define SG_ESC_BKT 32
+#endif
+  int lnb = ceil_log2((unsigned)((u + SG_ESC_BKT - 1) / SG_ESC_BKT));  // ~SG_ESC_BKT products per bucket
   lnb = max(lnb, kb + pb - 32);
   lnb = min(lnb, ceil_log2(Smem<CAP, V>::NBMAX));
   lnb = min(lnb, kb);

@@ -17,9 +17,11 @@ def _reset_debug():
     import paper_1504_05022_b200 as sg
     sg.set_debug(-1, 0, 0)
     sg.set_debug_long_tile(0)
+    sg.set_debug_long_bucket(0)
     yield
     sg.set_debug(-1, 0, 0)
     sg.set_debug_long_tile(0)
+    sg.set_debug_long_bucket(0)
 
 
 def _exact(g, R):
@@ -57,6 +59,7 @@ def test_f32_long_multi_tile(flags_name):
     A = gen.random_rows(40, 2000, np.array([3, 20, 100, 300] * 10), seed=42, mode="real")
     sg.set_debug(-1, 64, 40)
     sg.set_debug_long_tile(8192)
+    sg.set_debug_long_bucket(-1)  # the multi-tile rank / progressive path for every long row
     g = run_gpu(A, B, flags=getattr(sg, flags_name) if flags_name else 0, stats=True, fp32=True)
     assert g["stats"]["long_rows"] > 0
     _exact(g, oracle.spgemm(A, B, fp32=True))
@@ -86,3 +89,16 @@ def test_f32_api_guards():
     c = torch.empty(11, dtype=torch.int64, device="cuda")
     assert lib.spgemm_numeric(op.h, c.data_ptr(), None, None) == 1   # fp64 numeric on an fp32 handle
     op.destroy()
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+def test_f32_long_bucket_path(flags_name):
+    """SpSGEMM long rows on the bucket path (every long row, via the knob)."""
+    import paper_1504_05022_b200 as sg
+    B = gen.random_rows(2000, 400_000, np.full(2000, 64), seed=41, mode="real")
+    A = gen.random_rows(40, 2000, np.array([3, 20, 100, 300] * 10), seed=42, mode="real")
+    sg.set_debug(-1, 0, 40)
+    sg.set_debug_long_bucket(1)
+    g = run_gpu(A, B, flags=getattr(sg, flags_name) if flags_name else 0, stats=True, fp32=True)
+    assert g["stats"]["tier_rows"].get("long", 0) > 0
+    _exact(g, oracle.spgemm(A, B, fp32=True))

@@ -409,6 +409,7 @@ def test_long_multi_tile(flags_name, mode):
     A = gen.random_rows(60, 2000, np.array([1, 3, 10, 20, 40, 100, 300] * 8 + [2, 5, 7, 9]), seed=32, mode=mode)
     sg.set_debug(-1, 0, 40)          # every row with min(u, n) > 40 takes the long path
     sg.set_debug_long_tile(8192)     # tiles of 8 Ki (values) / 16 Ki (count) columns
+    sg.set_debug_long_bucket(-1)     # wide windows too (the bucket path: test_long_bucket_path)
     g = run_gpu(A, B, flags=flags, stats=True)
     g2 = run_gpu(A, B, flags=flags)
     R = oracle.spgemm(A, B)
@@ -519,3 +520,31 @@ def test_long_bucket_path(mode, min_window, flags_name):
     np.testing.assert_array_equal(g["ci"], R.ci)
     np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
     np.testing.assert_array_equal(g2["val"].view(np.int64), g["val"].view(np.int64))
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+def test_window_class_relaxed_bound(flags_name):
+    """Precise strategy: rows with 2048 < min(u, W) <= 8192 and W <= 2^17 start in the window
+    class; after the count, those longer than 2048 leave it for the ESC / CTA classes, the rest
+    (columns repeated by many b_j*) keep the dense accumulator.  Hybrid keeps the strict bound.
+    Structure exact, values bit for bit against the oracle."""
+    import paper_1504_05022_b200 as sg
+    flags = getattr(sg, flags_name) if flags_name else 0
+    n = 100_000
+    Bw = gen.random_rows(300, n, np.full(300, 20), seed=61, mode="real")       # spread columns
+    Bn = gen.random_rows(300, 600, np.full(300, 40), seed=62, mode="real")     # 600-column band
+    off = np.zeros(300, dtype=np.int64) + 50_000
+    rp = np.concatenate([Bw.rp, Bw.rp[-1] + Bn.rp[1:]])
+    ci = np.concatenate([Bw.ci, Bn.ci + off[0]]).astype(np.int32)
+    B = gen.Csr((600, n), rp, ci, np.concatenate([Bw.val, Bn.val]))
+    rows, cols = [], []
+    for i in range(40):
+        js = np.arange(0, 300, 1 + i % 3) if i % 2 == 0 else np.arange(300, 600, 1 + i % 3)
+        rows += [i] * len(js)
+        cols += list(js)
+    A = gen.with_values(gen.from_coo(np.array(rows), np.array(cols), (40, 600)), "real", 63)
+    g = run_gpu(A, B, flags=flags, stats=True)
+    R = oracle.spgemm(A, B)
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
