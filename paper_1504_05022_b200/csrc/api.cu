@@ -660,6 +660,7 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
       a.mode = MODE_DENSE;
       a.struct_col = h->ctil_col;
       a.struct_off = ws.ctil_off;
+      a.row_len = h->nnz_row;  // C~ offsets are capacities here
       a.nnz_row = nullptr;
       a.bw_vmax = h->pinned[kSumVmax];
       a.bw_bmax = h->pinned[kSumBmax];

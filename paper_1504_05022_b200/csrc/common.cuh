@@ -232,6 +232,7 @@ struct Stage3Args {
   double* out_val;
   int64_t* nnz_row;        // per-row nnz (written in both modes; may be NULL in numeric)
   int mode;
+  const int64_t* row_len;     // DENSE: nnz(c_i*) by row when out_off holds capacities (hybrid C~)
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
   const int32_t* rlo;         // first column of each row's window (stage 1)

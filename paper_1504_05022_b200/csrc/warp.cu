@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     if (MODE == MODE_DENSE) {
       // the sorted column set from the symbolic pass: slots of the nonzero blocks in column
       // order, bits, ranks, and C's columns directly
-      nnz = (int)(__ldg(a.out_off + row + 1) - o);
+      nnz = (int)(a.row_len ? __ldg(a.row_len + row) : __ldg(a.out_off + row + 1) - o);
       const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
       int prevd = -1;  // d of the previous chunk's last column
       for (int p0 = 0; p0 < nnz; p0 += 32) {
