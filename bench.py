@@ -403,16 +403,16 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
         if not hybrid:
             sym_ms = st0["stage_ms"][1]
             alg = 16 * m0 + 4 * dA0.nnz + 4 * min(Bm0.nnz, st0["sum_u"])
-            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bw_struct2 / k_wrow / k_cta_hash COUNT / "
+            cands.append((sym_ms, alg, "%s: symbolic stage-3 pass (k_bw_sym / k_wrow / k_cta_hash / "
                           "k_long_bm_count)" % name0, "symbolic"))
         for cls_name, c in st0["classes"].items():
             if c["ms"] <= 0:
                 continue
             alg = 16 * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + 12 * c["c_entries"]
-            kname = ("k_bwrow DENSE" if not hybrid else "k_bw_struct2 FILL") if cls_name == "bw" else \
-                "k_esc_merge" if cls_name.startswith("w") else \
-                "k_group" if cls_name.startswith("g") else "k_esc_sort / k_esc_merge" if cls_name.startswith("e") else \
-                "k_long_rank" if cls_name.startswith("c") else ("k_long + k_long_rank" if hybrid else "k_long_rank")
+            kname = ("k_bwrow DENSE" if not hybrid else "k_bw_sym + k_bwrow DENSE") if cls_name == "bw" else \
+                "k_esc_bk" if cls_name.startswith(("w", "e")) else \
+                "k_group" if cls_name.startswith("g") else \
+                "k_long_rank" if cls_name.startswith("c") else "k_bk_part/sort/copy + k_long_rank"
             cands.append((c["ms"], alg, "%s: stage-3 class %s (%s)" % (name0, cls_name, kname), cls_name))
     best = max(cands, key=lambda x: x[0])
     launch_ms, alg, kern, cls_name = best
