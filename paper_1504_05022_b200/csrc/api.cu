@@ -345,6 +345,7 @@ spgemm_status_t run_long(spgemm_handle_t h) {
   AL(h, &h->lsizes, nl);
   AL(h, &h->loff, nl + 1);
   AL(h, &h->ltable, nl * kMaxChunks);
+  CK(h, cudaMemsetAsync(h->ltable, 0, sizeof(int64_t) * nl * kMaxChunks, h->stream));  // (read whole, used by prefix)
   AL(h, &h->work_ctr, 1);
   int64_t c0 = 1;
   h->log2c0 = 0;

@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
       sh_stv(va, Arith<V>::add(sh_ldv<V>(va), Arith<V>::mul(at, v)));
+      __syncwarp();  // the next step's lanes may read this slot (memory-model order, not just lockstep)
     };
     if (MODE == MODE_DENSE) walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
     else walk_row<true, IT, V>(a, a0, a1, lane, accumulate);
