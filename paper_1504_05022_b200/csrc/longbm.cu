@@ -255,12 +255,11 @@ __global__ void __launch_bounds__(kBmNT) k_long_bm_count(Stage3Args a, int tmax)
 // (earlier tiles stay written), reports how much it needs, and resumes at that tile after the
 // host has grown its allocation.
 template <int NT, bool PROG, typename VT>
-__global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V) {
+__global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned* bm = reinterpret_cast<unsigned*>(smem);
   int* pre = reinterpret_cast<int*>(smem + size_t(tmax) * sizeof(unsigned));
-  VT* vals = reinterpret_cast<VT*>(smem + size_t(tmax) * 8);  // V values of a rank window
   __shared__ int s_red[2 * NW];
   __shared__ int s_w[NW + 1];
   __shared__ Batch<NT> sb;
@@ -351,9 +350,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
       // 3. values.  The tile's ranks are split into NW equal ranges: warp k owns the ranks
       //    [floor(k*T/NW), floor((k+1)*T/NW)), i.e. the columns [cb[k], cb[k+1]); every warp
       //    walks the a_ij in j-ascending order and adds, of each b_j*, only the products of its
-      //    own columns.  The values accumulate in shared memory when the tile's T entries fit
-      //    (V of them), else in place in the output (L2).
-      const bool insm = T <= V;
+      //    own columns.  The values accumulate in place in the output (L2).
       {
         const int w0 = 0, wn = T;
         for (int k = 0; k <= NW; ++k) {
@@ -375,10 +372,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
             }
           }
         }
-        for (int i = threadIdx.x; i < wn; i += NT) {  // the identity of + (line 9's assignment)
-          if (insm) vals[i] = VT(-0.0);
-          else ov[at_pos(done + i)] = VT(-0.0);
-        }
+        for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + i)] = VT(-0.0);  // identity of + (line 9)
         __syncthreads();
         for (int64_t e0 = a0; e0 < a1; e0 += NT) {
           const int64_t e = e0 + threadIdx.x;
@@ -456,32 +450,21 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax, int V)
                   x[u] = pre[wd] + __popc(bm[wd] & ((1u << (d & 31)) - 1u)) - w0;
                 }
               }
-              if (insm) {
+              VT* p[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) old[u] = vals[x[u]];
+              for (int u = 0; u < 4; ++u)
+                if (x[u] >= 0) {
+                  p[u] = ov + at_pos(done + x[u]);
+                  old[u] = *p[u];
+                }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) vals[x[u]] = Arith<VT>::add(old[u], Arith<VT>::mul(at, v[u]));  // lines 6, 9, 11
-              } else {
-                VT* p[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) {
-                    p[u] = ov + at_pos(done + x[u]);
-                    old[u] = *p[u];
-                  }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (x[u] >= 0) *p[u] = Arith<VT>::add(old[u], Arith<VT>::mul(at, v[u]));
-              }
+              for (int u = 0; u < 4; ++u)
+                if (x[u] >= 0) *p[u] = Arith<VT>::add(old[u], Arith<VT>::mul(at, v[u]));  // lines 6, 9, 11
             }
             __syncwarp();  // the next segment may add into a column this one just wrote
           }
           __syncthreads();
         }
-        if (insm)
-          for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + w0 + i)] = vals[i];
         __syncthreads();
       }
       done += T;
@@ -587,8 +570,6 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   // tiles never exceed the column range [0, n)
   const int64_t nwords = round_up((a.n + 31) / 32 + 1, nt);
   int64_t tmax = fill ? kDefaultRankTileWords : kDefaultCountTileWords;
-  static const int64_t env_tw = getenv("SPGEMM_LONG_TILE_WORDS") ? atoll(getenv("SPGEMM_LONG_TILE_WORDS")) : 0;
-  if (env_tw > 0) tmax = env_tw;
   if (g_long_tile_words > 0) tmax = g_long_tile_words;
   tmax = round_up(tmax, nt);
   if (tmax > nwords) tmax = nwords;
@@ -598,29 +579,14 @@ cudaError_t launch_long_bitmap(const Stage3Args& a, cudaStream_t s) {
   if (fill) {
     auto kern = a.f32 ? (a.lst ? k_long_rank<kRkNT, true, float> : k_long_rank<kRkNT, false, float>)
                       : (a.lst ? k_long_rank<kRkNT, true, double> : k_long_rank<kRkNT, false, double>);
-    // two CTAs per SM: the rest of a CTA's share of shared memory holds the values of a rank
-    // window (c3b: 64 KB of bits and ranks, 4 Ki values)
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    int dev = 0, smem_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    static const int ctas = getenv("SPGEMM_RANK_CTAS") ? atoi(getenv("SPGEMM_RANK_CTAS")) : 2;
-    const int64_t per_cta = int64_t(smem_sm) / (ctas > 0 ? ctas : 2) - 1024 - int64_t(fa.sharedSizeBytes);
-    int64_t V = (per_cta - int64_t(sm)) / 8 / 256 * 256;
-    if (V < 1024) V = 1024;
-    // shared accumulation for tiles of at most V entries measured slower on c3b (70 vs 51 ms)
-    static const int use_smem = getenv("SPGEMM_RANK_SMEM") ? atoi(getenv("SPGEMM_RANK_SMEM")) : 0;
-    if (!use_smem) V = 0;  // every tile accumulates in place in the output (L2)
-    const size_t smv = sm + size_t(V) * 8;
+    const size_t smv = sm;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);
     if (e != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smv);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = int64_t(sm_count()) * per_sm;
     if (grid > a.count) grid = a.count;
-    kern<<<(unsigned)grid, nt, smv, s>>>(a, (int)tmax, (int)V);
+    kern<<<(unsigned)grid, nt, smv, s>>>(a, (int)tmax);
   } else {
     e = cudaFuncSetAttribute(k_long_bm_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -320,18 +320,12 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
     off = (off + 15u) & ~15u;
     L.o_stage = off;         // a_ij chunk records of walk_row_staged
     off += 512u;
-  } else {
+  } else {  // STRUCT: bitmap + summary
     L.o_stage = 0;
-    const bool fill = mode == MODE_FILL;
     off = 4u * L.nwd;
     L.o_sm = off;
-    if (mode != MODE_COUNT) off += 4u * L.nsw;
-    L.o_pre = off;
-    if (fill) off += 2u * L.nwd;
-    L.o_lst = off;
-    if (fill) off += 4u * L.nvp;
-    L.o_vals = off;
-    if (fill) off += 8u * (L.nv + 1);  // + scratch
+    off += 4u * L.nsw;
+    L.o_pre = L.o_lst = L.o_vals = off;
   }
   L.bytes = (off + 15u) & ~15u;
   return L;
@@ -339,7 +333,7 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
 
 template <int MODE, typename IT, typename V>
 __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
-  constexpr bool SUMM = MODE == MODE_STRUCT || MODE == MODE_FILL;  // products -> bits + summary
+  static_assert(MODE == MODE_STRUCT || MODE == MODE_DENSE, "window class: STRUCT or DENSE");
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nwd = L.nwd, nsw = L.nsw;
@@ -352,12 +346,11 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
   int bmax = 0;  // STRUCT: most nonzero 1024-column blocks in one row (sizes DENSE's slots)
 
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.count;
-  // STRUCT / COUNT: each CTA takes a contiguous range of the class's rows (ascending row
-  // ids): neighbouring rows share b_j*, reused from L1.  FILL (hybrid) and DENSE keep the
-  // strided order: FILL's large per-warp buffers leave little L1 (contiguous was 30 % slower);
-  // DENSE runs in the same time either way, but strided rows keep a 3D stencil's z-neighbours
-  // in L2 (c2 DRAM reads 2.7 GB instead of 7.5 GB, ≈ the algorithmic bytes).
-  const bool contig = MODE != MODE_FILL && MODE != MODE_DENSE;
+  // STRUCT: each CTA takes a contiguous range of the class's rows (ascending row ids):
+  // neighbouring rows share b_j*, reused from L1.  DENSE keeps the strided order: it runs in
+  // the same time either way, but strided rows keep a 3D stencil's z-neighbours in L2 (c2 DRAM
+  // reads 2.7 GB instead of 7.5 GB, ≈ the algorithmic bytes).
+  const bool contig = MODE != MODE_DENSE;
   const int64_t per = contig ? (count + gridDim.x - 1) / gridDim.x : count;
   const int64_t rend = contig ? min(int64_t(blockIdx.x) * per + per, count) : count;
   const int64_t rstep = contig ? nw : int64_t(gridDim.x) * nw;
@@ -375,29 +368,9 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       walk_row<false, IT, V>(a, a0, a1, lane, [=](int c, V, V, bool act) {
         const unsigned d = act ? (unsigned)(c - lo) : 0u;
         const unsigned wa = bm + ((d >> 5) << 2);
-        if (SUMM) {
-          if (sh_atom_or(wa, 1u << (d & 31)) == 0u) sh_red_or(sm + ((d >> 10) << 2), 1u << ((d >> 5) & 31));
-        } else {
-          sh_red_or(wa, 1u << (d & 31));
-        }
+        if (sh_atom_or(wa, 1u << (d & 31)) == 0u) sh_red_or(sm + ((d >> 10) << 2), 1u << ((d >> 5) & 31));
       });
       __syncwarp();
-    }
-    if (MODE == MODE_COUNT) {
-      // popcount of the window, clearing the words that were set
-      int cnt = 0;
-      for (int q = lane; q < nwd / 4; q += 32) {
-        const int4 x = sh_ld_v4(bm + 16u * q);
-        if ((x.x | x.y | x.z | x.w) != 0) {
-          cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-          sh_st_v4_zero(bm + 16u * q);
-        }
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
-      if (lane == 0 && a.nnz_row) a.nnz_row[row] = cnt;
-      __syncwarp();
-      continue;
     }
     if (MODE == MODE_STRUCT) {
       // the sorted column set, block by nonzero block (clears bitmap and summary)
@@ -430,41 +403,6 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
       if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
       __syncwarp();
       continue;
-    }
-    int nl = 0;
-    if (MODE == MODE_FILL) {
-      // nonzero words in ascending order (clears the summary)
-      for (int s0 = 0; s0 < nsw; s0 += 32) {
-        const int s = s0 + lane;
-        unsigned sw = sh_ld(sm + 4u * s);
-        if (sw) sh_st(sm + 4u * s, 0u);
-        const int pc = __popc(sw);
-        const int inc = warp_incl_scan(pc, lane);
-        int pos = nl + inc - pc;
-        while (sw) {
-          sh_st(lst + 4u * pos++, unsigned(s * 32 + __ffs(sw) - 1));
-          sw &= sw - 1;
-        }
-        nl += __shfl_sync(kFull, inc, 31);
-      }
-      __syncwarp();
-      // ranks of the nonzero words; the row's columns in order (no sort)
-      int32_t* oc = a.out_col + o;
-      for (int q0 = 0; q0 < nl; q0 += 32) {
-        const int q = q0 + lane;
-        const int wd = q < nl ? (int)sh_ld(lst + 4u * q) : 0;
-        unsigned word = q < nl ? sh_ld(bm + 4u * wd) : 0u;
-        const int pc = __popc(word);
-        const int inc = warp_incl_scan(pc, lane);
-        int p = nnz + inc - pc;
-        if (q < nl) sh_st_u16(pre + 2u * wd, (unsigned)p);
-        const int cb = lo + wd * 32;
-        while (word) {
-          oc[p++] = cb + __ffs(word) - 1;
-          word &= word - 1;
-        }
-        nnz += __shfl_sync(kFull, inc, 31);
-      }
     }
     const unsigned dir = sm, bits = lst;  // DENSE names
     int nslot = 0;
@@ -516,33 +454,20 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
     const unsigned scratch = vals + 8u * unsigned(L.nv);
     auto accumulate = [=](int c, V v, V at, bool act) {
       const unsigned d = act ? (unsigned)(c - lo) : 0u;
-      unsigned word, base;
-      if (MODE == MODE_DENSE) {  // one 8-byte record: the word's bits and its first rank
-        // record (d>>5)%32 of slot dir-1: bits + (dir-1)*kRecSlot + ((d >> 2) & 0xf8)
-        const uint2 rec = sh_ld_v2(bits - kRecSlot + sh_ld_u16(dir + 2u * (d >> 10)) * kRecSlot + ((d >> 2) & 0xf8u));
-        word = rec.x;
-        base = rec.y;
-      } else {
-        const unsigned wi = d >> 5;
-        word = sh_ld(bm + 4u * wi);
-        base = sh_ld_u16(pre + 2u * wi);
-      }
-      const unsigned rank = base + __popc(word & ((1u << (d & 31)) - 1u));
+      // one 8-byte record: the word's bits and its first rank;
+      // record (d>>5)%32 of slot dir-1: bits + (dir-1)*kRecSlot + ((d >> 2) & 0xf8)
+      const uint2 rec = sh_ld_v2(bits - kRecSlot + sh_ld_u16(dir + 2u * (d >> 10)) * kRecSlot + ((d >> 2) & 0xf8u));
+      const unsigned rank = rec.y + __popc(rec.x & ((1u << (d & 31)) - 1u));
       const unsigned va = act ? vals + 8u * rank : scratch;
       sh_stv(va, Arith<V>::add(sh_ldv<V>(va), Arith<V>::mul(at, v)));
       __syncwarp();  // the next step's lanes may read this slot (memory-model order, not just lockstep)
     };
-    if (MODE == MODE_DENSE) walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
-    else walk_row<true, IT, V>(a, a0, a1, lane, accumulate);
+    walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
     __syncwarp();
     V* ov = vcast<V>(a.out_val) + o;
     for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
-    if (MODE == MODE_FILL) {
-      for (int q = lane; q < nl; q += 32) sh_st(bm + 4u * sh_ld(lst + 4u * q), 0u);
-    } else {
-      for (int s = 0; s < nslot; ++s) sh_st(bits + unsigned(s) * kRecSlot + 8u * lane, 0u);
-      for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
-    }
+    for (int s = 0; s < nslot; ++s) sh_st(bits + unsigned(s) * kRecSlot + 8u * lane, 0u);
+    for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
     __syncwarp();
   }
@@ -558,34 +483,30 @@ __global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
 // Per warp: dir uint16[nsw] (block -> slot + 1) | bits uint32[ns·32].  ~2.3 KB per warp
 // instead of W/8: 2x the resident warps on c2.  Inserting is a fire-and-forget shared OR.
 // A row touching more than ns blocks is appended to an overflow list and redone by the
-// full-window kernel.  FILL (hybrid) continues like the DENSE numeric kernel: ranks per word
-// from the emission, a second walk adds each product at its rank (c2 hybrid 20.3 -> 15.0 ms).
-// FILL (hybrid) adds pre uint16[ns·32] (rank of each word's first bit) and vals double[nv+1].
+// full-window kernel.  (64-bit B offsets; k_bw_sym below is the 32-bit version.)
 struct Bs2Layout {
-  int nsw, ns, nv;
-  unsigned o_bits, o_pre, o_vals, o_stage, bytes;
+  int nsw, ns;
+  unsigned o_bits, o_pre, o_stage, bytes;
 };
 
-__host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns, bool fill, int64_t vmax) {
+__host__ __device__ inline Bs2Layout bs2_layout(int64_t wmax, int ns) {
   Bs2Layout L;
   const int nwd = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024 * 32);
   L.nsw = (nwd / 32 + 31) / 32 * 32;
   L.ns = ns;
-  L.nv = (int)(vmax > 0 ? vmax : 1);
   L.o_bits = (2u * L.nsw + 15u) & ~15u;
   L.o_pre = L.o_bits + 128u * ns;
-  L.o_vals = L.o_pre + (fill ? 64u * ns : 0u);
-  L.o_stage = fill ? ((L.o_vals + 8u * (L.nv + 1) + 15u) & ~15u) : L.o_pre;  // o_pre is 16-aligned
+  L.o_stage = L.o_pre;         // o_pre is 16-aligned
   L.bytes = L.o_stage + 512u;  // a_ij chunk records of walk_row_staged
   return L;
 }
 
-template <typename IT, bool FILL, typename V>
+template <typename IT, typename V>
 __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
-  const unsigned bits = dir + L.o_bits, pre = dir + L.o_pre, vals = dir + L.o_vals;
+  const unsigned bits = dir + L.o_bits;
   const unsigned stage = dir + L.o_stage, bitsm = bits - 128u;
   const int ns = L.ns, nsw = L.nsw;
   for (unsigned i = lane; i < L.o_pre / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
@@ -635,18 +556,17 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
     for (int s0 = 0; s0 < nsw; s0 += 32) {
       const unsigned dl = sh_ld_u16(dir + 2u * (s0 + lane));
       unsigned nzb = __ballot_sync(kFull, dl != 0u);
-      if (!FILL && dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
+      if (dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
       while (nzb) {
         const int b = __ffs(nzb) - 1;
         nzb &= nzb - 1;
         const unsigned slot = __shfl_sync(kFull, dl, b) - 1u;
         const unsigned wa = bits + 4u * (slot * 32u + lane);
         unsigned word = sh_ld(wa);
-        if (!FILL && word) sh_st(wa, 0u);
+        if (word) sh_st(wa, 0u);
         const int pc = __popc(word);
         const int inc = warp_incl_scan(pc, lane);
         int p = nnz + inc - pc;
-        if (FILL) sh_st_u16(pre + 2u * (slot * 32u + lane), (unsigned)p);
         const int cb = lo + ((s0 + b) * 32 + lane) * 32 - 1;
         int32_t* q = oc + p;
         while (word) {
@@ -655,25 +575,6 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
         }
         nnz += __shfl_sync(kFull, inc, 31);
       }
-    }
-    if (FILL) {
-      // lines 6, 9, 11: values at the columns' ranks (as the DENSE numeric kernel), then clear
-      for (int p = lane; p < nnz; p += 32) sh_stv(vals + 8u * p, V(-0.0));
-      __syncwarp();
-      const unsigned scratch = vals + 8u * unsigned(L.nv);
-      walk_row<true, IT, V>(a, a0, a1, lane, [=](int c, V v, V at, bool act) {
-        const unsigned d = act ? (unsigned)(c - lo) : 0u;
-        const unsigned wi = (sh_ld_u16(dir + 2u * (d >> 10)) - 1u) * 32u + ((d >> 5) & 31u);
-        const unsigned word = sh_ld(bits + 4u * wi);
-        const unsigned rank = sh_ld_u16(pre + 2u * wi) + __popc(word & ((1u << (d & 31)) - 1u));
-        const unsigned va = act ? vals + 8u * rank : scratch;
-        sh_stv(va, Arith<V>::add(sh_ldv<V>(va), Arith<V>::mul(at, v)));
-      });
-      __syncwarp();
-      V* ov = vcast<V>(a.out_val) + o;
-      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
-      for (int sl = 0; sl < nslot; ++sl) sh_st(bits + 4u * (unsigned(sl) * 32u + lane), 0u);
-      for (int q = lane; q < nsw / 8; q += 32) sh_st_v4_zero(dir + 16u * q);
     }
     bmax = max(bmax, nslot);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
@@ -697,7 +598,6 @@ __global__ void __launch_bounds__(256) k_bw_struct2(Stage3Args a, Bs2Layout L) {
 struct SymLayout {
   int nsw, ns;
   unsigned o_bits, o_stage, bytes;
-  int combine;  // combine the bits of a run's lanes before the RED (or_runs)
 };
 // slots of 33 words: the same word of different slots (a stencil's z-neighbour planes) lands in
 // different banks
@@ -712,23 +612,6 @@ __host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
   L.o_stage = (L.o_bits + kSlotBytes * (ns + 1) + 15u) & ~15u;
   L.bytes = L.o_stage + 512u;
   return L;
-}
-
-// OR the bit of every active lane into its word (the lanes of one b_j* step hold sorted
-// columns, so lanes sharing a word form contiguous runs): the bits of up to four consecutive
-// lanes of a run are combined with two shuffles and one lane of each group of four issues the
-// RED — c2's runs of three cost one RED instead of three same-address ones.
-__device__ __forceinline__ void or_runs(unsigned addr, unsigned bit, bool act, unsigned le, int lane) {
-  const unsigned key = act ? addr : 0xffffffe0u + lane;  // idle lanes: unique, never shared
-  unsigned v = act ? bit : 0u;
-  const unsigned k1 = __shfl_down_sync(kFull, key, 1), v1 = __shfl_down_sync(kFull, v, 1);
-  if (k1 == key && lane < 31) v |= v1;
-  const unsigned k2 = __shfl_down_sync(kFull, key, 2), v2 = __shfl_down_sync(kFull, v, 2);
-  if (k2 == key && lane < 30) v |= v2;
-  const unsigned kp = __shfl_up_sync(kFull, key, 1);
-  const unsigned S = __ballot_sync(kFull, lane == 0 || kp != key);  // run starts
-  const unsigned pos = lane - (31u - __clz(S & le));                // position in the run
-  if (act && (pos & 3u) == 0u) sh_red_or(addr, v);
 }
 
 __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
@@ -830,15 +713,9 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
           }
         }
         // line 8 of Algorithm 1: set the column's bit (idle lanes and slot-less rows: no RED)
-        if (L.combine) {
 #pragma unroll
-          for (int u = 0; u < kGroup; ++u)
-            or_runs(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), 1u << (d[u] & 31), sl[u] != 0u, le, lane);
-        } else {
-#pragma unroll
-          for (int u = 0; u < kGroup; ++u)  // idle lanes and slot-less rows: OR 0 into the dummy slot
-            sh_red_or(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), sl[u] ? 1u << (d[u] & 31) : 0u);
-        }
+        for (int u = 0; u < kGroup; ++u)  // idle lanes and slot-less rows: OR 0 into the dummy slot
+          sh_red_or(bits + sl[u] * kSlotBytes + ((d[u] >> 3) & 0x7cu), sl[u] ? 1u << (d[u] & 31) : 0u);
       }
     }
     __syncwarp();
@@ -957,7 +834,7 @@ template <int MODE>
 static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
   const BwLayout L = bw_layout(MODE, a.bw_wmax, a.bw_vmax, a.bw_bmax);
   const bool i32 = a.b_nnz < (int64_t(1) << 31);
-  const bool f32 = a.f32 && (MODE == MODE_FILL || MODE == MODE_DENSE);
+  const bool f32 = a.f32 && MODE == MODE_DENSE;
   auto kern = f32 ? (i32 ? k_bwrow<MODE, int, float> : k_bwrow<MODE, int64_t, float>)
                   : (i32 ? k_bwrow<MODE, int, double> : k_bwrow<MODE, int64_t, double>);
   int best_nw = 1, best_warps = 0;
@@ -987,10 +864,10 @@ static cudaError_t launch_bw_mode(const Stage3Args& a, cudaStream_t s) {
 
 constexpr int kBs2Slots = 16;
 
-template <typename IT, bool FILL>
+template <typename IT>
 static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
-  const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots, FILL, a.bw_vmax);
-  auto kern = (FILL && a.f32) ? k_bw_struct2<IT, FILL, float> : k_bw_struct2<IT, FILL, double>;
+  const Bs2Layout L = bs2_layout(a.bw_wmax, kBs2Slots);
+  auto kern = k_bw_struct2<IT, double>;
   constexpr int nw = 8;
   const size_t bytes = size_t(nw) * L.bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1006,9 +883,7 @@ static cudaError_t launch_bs2(const Stage3Args& a, cudaStream_t s) {
 }
 
 static cudaError_t launch_sym(const Stage3Args& a, cudaStream_t s) {
-  SymLayout L = sym_layout(a.bw_wmax, kBs2Slots);
-  static const int combine = getenv("SPGEMM_SYM_COMBINE") ? atoi(getenv("SPGEMM_SYM_COMBINE")) : 0;
-  L.combine = combine;
+  const SymLayout L = sym_layout(a.bw_wmax, kBs2Slots);
   constexpr int nw = 8;
   const size_t bytes = size_t(nw) * L.bytes;
   cudaError_t e = cudaFuncSetAttribute(k_bw_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1023,34 +898,28 @@ static cudaError_t launch_sym(const Stage3Args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Window class: STRUCT (the sorted column sets: block directory first, the full window for
+// rows with more nonzero blocks than slots) or DENSE (values by rank from those sets).
 cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const int64_t blocks = (a.bw_wmax + 1023) / 1024;
-  static const bool no_bs2 = getenv("SPGEMM_NO_BS2") != nullptr;  // A/B switch (development)
-  const bool dir_mode = a.mode == MODE_STRUCT || a.mode == MODE_FILL;
-  if (dir_mode && blocks > kBs2Slots && a.bw_ovf_list && a.bw_ovf_cnt && !no_bs2) {
+  if (a.mode == MODE_DENSE) return launch_bw_mode<MODE_DENSE>(a, s);
+  if (a.mode != MODE_STRUCT) return cudaErrorInvalidValue;
+  if (blocks > kBs2Slots && a.bw_ovf_list && a.bw_ovf_cnt) {
     // block-directory pass, then the full-window pass over the rows that overflowed it
     cudaError_t e = cudaMemsetAsync(a.bw_ovf_cnt, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     const bool i32 = a.b_nnz < (int64_t(1) << 31);
-    const bool fill = a.mode == MODE_FILL;
-    static const bool old_sym = getenv("SPGEMM_OLD_SYM") != nullptr;  // A/B switch (development)
-    e = fill ? (i32 ? launch_bs2<int, true>(a, s) : launch_bs2<int64_t, true>(a, s))
-             : (i32 ? (old_sym ? launch_bs2<int, false>(a, s) : launch_sym(a, s)) : launch_bs2<int64_t, false>(a, s));
+    e = i32 ? launch_sym(a, s) : launch_bs2<int64_t>(a, s);
     if (e != cudaSuccess) return e;
     Stage3Args b = a;
     b.perm = a.bw_ovf_list;
     b.first = 0;
     b.count = a.count;  // grid bound; the kernel reads the real count from count_dev
     b.count_dev = a.bw_ovf_cnt;
-    return fill ? launch_bw_mode<MODE_FILL>(b, s) : launch_bw_mode<MODE_STRUCT>(b, s);
+    return launch_bw_mode<MODE_STRUCT>(b, s);
   }
-  switch (a.mode) {
-    case MODE_FILL: return launch_bw_mode<MODE_FILL>(a, s);
-    case MODE_STRUCT: return launch_bw_mode<MODE_STRUCT>(a, s);
-    case MODE_DENSE: return launch_bw_mode<MODE_DENSE>(a, s);
-    default: return launch_bw_mode<MODE_COUNT>(a, s);
-  }
+  return launch_bw_mode<MODE_STRUCT>(a, s);
 }
 
 }  // namespace sg
