@@ -125,12 +125,23 @@ __device__ __forceinline__ void walk_row_staged(const int32_t* __restrict__ aci,
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(stage + 16u * (t0 + u)) : "memory");
           act[u] = lane < r.y;
+#ifndef SG_NO_CLAMP
+          // idle lanes load b_j*'s last entry (or entry 0 of B for an empty step): no
+          // predication, no default values; their result goes to a scratch slot (act)
+          const int q = r.x + min(lane, max(r.y - 1, 0));
+          c[u] = __ldg(bci + q);
+          if (VALS) {
+            at[u] = rec_val<V>(r);
+            v[u] = __ldg(bval + q);
+          }
+#else
           const int q = r.x + lane;
           c[u] = act[u] ? __ldg(bci + q) : kEmptyKey;
           if (VALS) {
             at[u] = rec_val<V>(r);
             v[u] = act[u] ? __ldg(bval + q) : V(0);
           }
+#endif
         }
 #pragma unroll
         for (int u = 0; u < kGroup; ++u) op(c[u], VALS ? v[u] : V(0), VALS ? at[u] : V(0), act[u]);
@@ -332,7 +343,10 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
 }
 
 template <int MODE, typename IT, typename V>
-__global__ void __launch_bounds__(256) k_bwrow(Stage3Args a, BwLayout L) {
+#ifndef SG_BW_MINB
+#define SG_BW_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayout L) {
   static_assert(MODE == MODE_STRUCT || MODE == MODE_DENSE, "window class: STRUCT or DENSE");
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;

@@ -548,3 +548,23 @@ def test_window_class_relaxed_bound(flags_name):
     np.testing.assert_array_equal(g["rp"], R.rp)
     np.testing.assert_array_equal(g["ci"], R.ci)
     np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_PRECISE", None])
+@pytest.mark.parametrize("mode", ["int", "real"])
+def test_rank_kernel_windows(flags_name, mode):
+    """Long rows with more than 16 Ki distinct columns in one bitmap tile: the rank kernel
+    accumulates their values one rank window (16 Ki ranks or T/4) at a time.  Rows of 28 Ki to
+    60 Ki entries (2-4 windows) next to short long rows; both strategies (hybrid: the
+    progressive path, windows of 200 000 columns <= one tile).  Bit for bit against the oracle."""
+    import paper_1504_05022_b200 as sg
+    flags = getattr(sg, flags_name) if flags_name else 0
+    B = gen.random_rows(1200, 200_000, np.full(1200, 100), seed=71, mode=mode)
+    A = gen.random_rows(12, 1200, np.array([300, 600, 40, 900] * 3), seed=72, mode=mode)
+    g = run_gpu(A, B, flags=flags, stats=True)
+    R = oracle.spgemm(A, B)
+    assert g["stats"]["tier_rows"].get("long", 0) >= 6
+    assert np.diff(R.rp).max() > 50_000
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
