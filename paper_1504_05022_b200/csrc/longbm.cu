@@ -34,7 +34,6 @@ constexpr int kRkNW = kRkNT / 32;
 constexpr int kDefaultCountTileWords = 32768;     // 1 Mi columns (128 KB)
 constexpr int kDefaultRankTileWords = 8192;       // 256 Ki columns (64 KB bits + 32 KB ranks)
 constexpr int kChunk = 256;                       // products per work item (load balance)
-constexpr int kRankWin = 16384;                   // rank kernel: values per window (L2 footprint)
 
 template <int NT>
 __device__ __forceinline__ int block_excl_scan_i(int v, int* total, int* s_w) {
@@ -351,13 +350,9 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
       // 3. values.  The tile's ranks are split into NW equal ranges: warp k owns the ranks
       //    [floor(k*T/NW), floor((k+1)*T/NW)), i.e. the columns [cb[k], cb[k+1]); every warp
       //    walks the a_ij in j-ascending order and adds, of each b_j*, only the products of its
-      //    own columns.  The values accumulate in place in the output (L2), one rank window
-      //    at a time: a window of at most max(kRankWin, T/4) ranks keeps every resident CTA's
-      //    read-modify-write footprint in L2 (c3b: 296 CTAs x 16 Ki values = 38 MB; a whole
-      //    135 Ki-entry row per CTA spilled the values to DRAM: 74 GB of traffic per launch).
-      const int WIN = max(kRankWin, (T + 3) / 4);
-      for (int w0 = 0; w0 < T; w0 += WIN) {
-        const int wn = min(WIN, T - w0);
+      //    own columns.  The values accumulate in place in the output (L2).
+      {
+        const int w0 = 0, wn = T;
         for (int k = 0; k <= NW; ++k) {
           const int rk = w0 + (k < NW ? (int)((int64_t(k) * wn) / NW) : wn);
           if (rk >= T) {
@@ -377,7 +372,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
             }
           }
         }
-        for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + w0 + i)] = VT(-0.0);  // identity of + (line 9)
+        for (int i = threadIdx.x; i < wn; i += NT) ov[at_pos(done + i)] = VT(-0.0);  // identity of + (line 9)
         __syncthreads();
         for (int64_t e0 = a0; e0 < a1; e0 += NT) {
           const int64_t e = e0 + threadIdx.x;
@@ -459,7 +454,7 @@ __global__ void __launch_bounds__(NT) k_long_rank(Stage3Args a, int tmax) {
 #pragma unroll
               for (int u = 0; u < 4; ++u)
                 if (x[u] >= 0) {
-                  p[u] = ov + at_pos(done + w0 + x[u]);
+                  p[u] = ov + at_pos(done + x[u]);
                   old[u] = *p[u];
                 }
 #pragma unroll
