@@ -55,7 +55,9 @@ for cfg in sys.argv[1:] or ["c2"]:
             totals[sname] = tot
             cells.append((st["workspace_bytes"], tot))
             if sname == "hybrid" and st["long_rows"] > 0:
-                cap = sum(min(c["products"], dB.cols) for k, c in st["classes"].items() if k == "long")
+                # the progressive arena against the long class's products (>= its upper bound
+                # sum of min(u_i, n)): growth never passes min(u_i, n), so no overshoot
+                cap = st["classes"]["long"]["products"]
                 arena = "%d of <= %d entries (0)" % (st["long_entries"], cap)
             if C is not None:
                 out = C
