@@ -127,6 +127,7 @@ struct spgemm_handle_s {
   int64_t* scan_tmp = nullptr;
   int32_t* ctil_col = nullptr;
   double* ctil_val = nullptr;
+  int32_t* bw_nw = nullptr;   // precise: words per window row's structure (-1: columns)
   int64_t* pinned = nullptr;  // host pinned scratch [kSumLen + 8]
   // long rows
   int64_t nlong = 0, long_first = 0;
@@ -216,6 +217,7 @@ void free_symbolic(spgemm_handle_t h) {
   h->nnz_row = h->c_rp = h->scan_tmp = nullptr;
   h->ctil_col = nullptr;
   h->ctil_val = nullptr;
+  h->bw_nw = nullptr;
   h->work_ctr = nullptr;
   h->lst = nullptr;
   h->lact = h->lovf = h->lovf_cnt = nullptr;
@@ -642,6 +644,11 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     if (t == T_BW) {
       AL(h, &a.bw_ovf_list, h->tier_count[T_BW]);
       AL(h, &a.bw_ovf_cnt, 1);
+      if (precise) {  // rows left at -1 (the full-window fallback) keep the column format
+        AL(h, &h->bw_nw, m);
+        CK(h, cudaMemsetAsync(h->bw_nw, 0xff, sizeof(int32_t) * m, h->stream));
+        a.bw_nw = h->bw_nw;
+      }
     }
     cudaEventRecord(h->tsym[t][0], h->stream);
     if (hybrid && t == T_BW) {
@@ -820,6 +827,7 @@ static spgemm_status_t spgemm_numeric_any(spgemm_handle_t h, int64_t* c_row_ptr,
         a.mode = dense ? MODE_DENSE : MODE_FILL;
         a.struct_col = h->ctil_col;
         a.struct_off = h->ws.ctil_off;
+        a.bw_nw = h->bw_nw;
         a.rlo = h->ws.rlo;
         a.bwin = h->ws.bwin;
         a.bw_wmax = h->bw_wmax;

@@ -178,12 +178,14 @@ __host__ __device__ inline int64_t hybrid_capacity(int t, int64_t u, int64_t n, 
   return u < n ? u : n;
 }
 // C~ capacity by strategy: CAP_HYBRID keeps whole rows (columns + values) in C~; CAP_PRECISE
-// keeps only the sorted column sets of the window-bitmap rows (STRUCT -> DENSE), no other row
-// needs C~ in the precise strategy.
+// keeps only the structure of the window-bitmap rows (STRUCT -> DENSE), no other row needs C~
+// in the precise strategy.  There the capacity is rounded up to even so every slice starts on
+// 8 bytes: STRUCT writes a row as its list of nonzero bitmap words ((first column, bits) pairs,
+// 8 B each) when that fits the slice, else as the sorted column set (4 B per entry).
 enum CapMode : int { CAP_NONE = 0, CAP_HYBRID = 1, CAP_PRECISE = 2 };
 __host__ __device__ inline int64_t ctil_capacity(int mode, int t, int64_t u, int64_t n, int64_t W, int64_t bk_min_w) {
   if (mode == CAP_HYBRID) return hybrid_capacity(t, u, n, W, bk_min_w);
-  if (mode == CAP_PRECISE && t == T_BW) return u < n ? u : n;
+  if (mode == CAP_PRECISE && t == T_BW) return ((u < n ? u : n) + 1) & ~int64_t(1);
   return 0;
 }
 
@@ -235,6 +237,8 @@ struct Stage3Args {
   const int64_t* row_len;     // DENSE: nnz(c_i*) by row when out_off holds capacities (hybrid C~)
   const int32_t* struct_col;  // DENSE: sorted column sets from STRUCT
   const int64_t* struct_off;  // DENSE: their per-row offsets
+  int32_t* bw_nw;             // precise T_BW: per row, the number of (first column, bits) words
+                              // STRUCT wrote (-1: the sorted column set instead); NULL: columns
   const int32_t* rlo;         // first column of each row's window (stage 1)
   const int32_t* rhi;         // last column of each row's window (stage 1)
   const int64_t* U;           // u_i of every row (stage 1)

@@ -306,7 +306,7 @@ __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
 //   vals double[nv]
 struct BwLayout {
   int nwd, nsw, nvp, nv, ns;
-  unsigned o_sm, o_pre, o_lst, o_vals, o_stage, bytes;  // per warp, bytes is a multiple of 16
+  unsigned o_sm, o_pre, o_lst, o_vals, o_stage, o_cols, bytes;  // per warp, bytes: multiple of 16
 };
 
 constexpr unsigned kRecSlot = 264u;  // DENSE: bytes per slot of 8-byte word records (33 records)
@@ -331,12 +331,16 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
     off = (off + 15u) & ~15u;
     L.o_stage = off;         // a_ij chunk records of walk_row_staged
     off += 512u;
+    L.o_cols = off;          // C's columns of a row given as words (written in order with vals)
+#ifdef SG_COLS_SMEM
+    off += 4u * L.nvp;
+#endif
   } else {  // STRUCT: bitmap + summary
     L.o_stage = 0;
     off = 4u * L.nwd;
     L.o_sm = off;
     off += 4u * L.nsw;
-    L.o_pre = L.o_lst = L.o_vals = off;
+    L.o_pre = L.o_lst = L.o_vals = L.o_cols = off;
   }
   L.bytes = (off + 15u) & ~15u;
   return L;
@@ -418,15 +422,62 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
       __syncwarp();
       continue;
     }
-    const unsigned dir = sm, bits = lst;  // DENSE names
-    int nslot = 0;
+    const unsigned dir = sm, bits = lst, cols = bm + L.o_cols;  // DENSE names
+    int nslot = 0, nwr = -1;
     if (MODE == MODE_DENSE) {
       // the sorted column set from the symbolic pass: slots of the nonzero blocks in column
       // order, bits, ranks, and C's columns directly
       nnz = (int)(a.row_len ? __ldg(a.row_len + row) : __ldg(a.out_off + row + 1) - o);
       const int32_t* sc = a.struct_col + __ldg(a.struct_off + row);
+      nwr = a.bw_nw ? __ldg(a.bw_nw + row) : -1;
+      if (nwr >= 0) {
+        // the row as its nonzero words (first column, bits), ascending: a word's record is
+        // {bits, rank of its first bit} with the rank from one scan of the popcounts; the
+        // columns go to the warp's column buffer at their ranks (written out with the values)
+        const uint2* sw = reinterpret_cast<const uint2*>(sc);
+        int prevb = -1, rank0 = 0;
+        for (int p0 = 0; p0 < nwr; p0 += 32) {
+          const int p = p0 + lane;
+          const bool in = p < nwr;
+          const uint2 ent = in ? __ldg(sw + p) : make_uint2(0u, 0u);
+          const int d = (int)ent.x - lo;  // a multiple of 32
+          const int blk = in ? d >> 10 : -1;
+          int bp = __shfl_up_sync(kFull, blk, 1);
+          if (lane == 0) bp = prevb;
+          const bool newblk = in && bp != blk;
+          const unsigned nm = __ballot_sync(kFull, newblk);
+          const int slot = nslot + __popc(nm & (lanemask_lt_() | (1u << lane))) - 1;
+          const int pc = __popc(ent.y);
+          const int inc = warp_incl_scan(pc, lane);
+          if (in) {
+            const int rank = rank0 + inc - pc;
+            if (newblk) sh_st_u16(dir + 2u * unsigned(blk), (unsigned)(slot + 1));
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(bits + unsigned(slot) * kRecSlot + 8u * ((d >> 5) & 31)),
+                         "r"(ent.y), "r"((unsigned)rank));
+            unsigned wd = ent.y;
+            const int cb = (int)ent.x - 1;
+#ifdef SG_COLS_SMEM
+            unsigned ca = cols + 4u * unsigned(rank);
+            while (wd) {
+              sh_st(ca, (unsigned)(cb + __ffs(wd)));
+              ca += 4u;
+              wd &= wd - 1;
+            }
+#else
+            int32_t* q = a.out_col + o + rank;
+            while (wd) {
+              *q++ = cb + __ffs(wd);
+              wd &= wd - 1;
+            }
+#endif
+          }
+          nslot += __popc(nm);
+          prevb = __shfl_sync(kFull, blk, 31);
+          rank0 += __shfl_sync(kFull, inc, 31);
+        }
+      }
       int prevd = -1;  // d of the previous chunk's last column
-      for (int p0 = 0; p0 < nnz; p0 += 32) {
+      for (int p0 = 0; nwr < 0 && p0 < nnz; p0 += 32) {
         const int p = p0 + lane;
         const bool in = p < nnz;
         const int c = in ? __ldg(sc + p) : 0;
@@ -479,7 +530,18 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
     walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
     __syncwarp();
     V* ov = vcast<V>(a.out_val) + o;
-    for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
+#ifdef SG_COLS_SMEM
+    if (nwr >= 0) {
+      int32_t* oc = a.out_col + o;
+      for (int p = lane; p < nnz; p += 32) {
+        oc[p] = (int)sh_ld(cols + 4u * p);
+        ov[p] = sh_ldv<V>(vals + 8u * p);
+      }
+    } else
+#endif
+    {
+      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
+    }
     for (int s = 0; s < nslot; ++s) sh_st(bits + unsigned(s) * kRecSlot + 8u * lane, 0u);
     for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
@@ -628,7 +690,10 @@ __host__ __device__ inline SymLayout sym_layout(int64_t wmax, int ns) {
   return L;
 }
 
-__global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
+#ifndef SG_SYM_MINB
+#define SG_SYM_MINB 6
+#endif
+__global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLayout L) {
   extern __shared__ __align__(16) uint32_t s_bw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
@@ -671,7 +736,8 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
           const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));  // lanes past the row: len 0
           nlong |= (int)rec.y > 32;
           const bool act = lane < (int)rec.y;
-          d[u] = act ? (unsigned)(__ldg(bci + (int)rec.x + lane) - lo) : 0u;
+          const int q = (int)rec.x + lane;  // 32-bit index: one IMAD.WIDE per gather
+          d[u] = act ? (unsigned)(__ldg(bci + q) - lo) : 0u;
           sl[u] = act ? sh_ld_u16(dir + 2u * (d[u] >> 10)) : 0u;  // 0: dummy slot / no slot yet
           need[u] = act && sl[u] == 0u;
         }
@@ -741,9 +807,48 @@ __global__ void __launch_bounds__(256) k_bw_sym(Stage3Args a, SymLayout L) {
       __syncwarp();
       continue;
     }
-    // the sorted column set: nonzero words in column order -> list (stage) -> bits
-    int32_t* oc = a.out_col + __ldg(a.out_off + row);
+    // the row's structure: nonzero words in column order -> list (stage) -> the row's slice,
+    // as the words themselves ((first column, bits) pairs: DENSE takes their ranks by one scan)
+    // when 8 B per word fits the slice, else as the sorted column set
+    const int64_t o = __ldg(a.out_off + row);
+    int32_t* oc = a.out_col + o;
+    bool words = false;
+    if (a.bw_nw) {
+      int nwt = 0;
+      for (int s = 1; s <= nslot; ++s) nwt += __popc(__ballot_sync(kFull, sh_ld(bits + s * kSlotBytes + 4u * lane) != 0u));
+      words = 2 * int64_t(nwt) <= __ldg(a.out_off + row + 1) - o;
+      if (lane == 0) a.bw_nw[row] = words ? nwt : -1;
+    }
     int nnz = 0, nl = 0;
+    if (words) {
+      // nonzero words straight to the slice in column order (coalesced 8-byte stores)
+      int nwo = 0;
+      unsigned pcs = 0;
+      for (int s0 = 0; s0 < nsw; s0 += 32) {
+        const unsigned dl = sh_ld_u16(dir + 2u * (s0 + lane));
+        unsigned nzb = __ballot_sync(kFull, dl != 0u);
+        if (dl) sh_st_u16(dir + 2u * (s0 + lane), 0u);
+        while (nzb) {
+          const int b = __ffs(nzb) - 1;
+          nzb &= nzb - 1;
+          const unsigned wa = bits + __shfl_sync(kFull, dl, b) * kSlotBytes + 4u * lane;
+          const unsigned word = sh_ld(wa);
+          const unsigned nzw = __ballot_sync(kFull, word != 0u);
+          if (word) {
+            sh_st(wa, 0u);
+            reinterpret_cast<uint2*>(oc)[nwo + __popc(nzw & lt)] =
+                make_uint2((unsigned)(lo + ((s0 + b) * 32 + lane) * 32), word);
+            pcs += __popc(word);
+          }
+          nwo += __popc(nzw);
+        }
+      }
+      nnz = (int)__reduce_add_sync(kFull, pcs);
+      bmax = max(bmax, nslot);
+      if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
+      __syncwarp();
+      continue;
+    }
     auto flush = [&](int cnt) {  // emit list entries [0, cnt) (cnt <= 32)
       uint2 ent = make_uint2(0u, 0u);
       if (lane < cnt) ent = sh_ld_v2(stage + 8u * lane);

@@ -568,3 +568,44 @@ def test_rank_kernel_large_tiles(flags_name, mode):
     np.testing.assert_array_equal(g["rp"], R.rp)
     np.testing.assert_array_equal(g["ci"], R.ci)
     np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp32", [False, True])
+def test_window_rows_word_and_column_structure(fp32):
+    """Precise strategy, window class: the structure pass stores a row as its nonzero bitmap
+    words ((first column, bits) pairs) when 8 B per word fits the row's slice, else as its
+    sorted columns.  Rows of clustered columns (many per word: word format) and rows whose
+    products land in distinct words with no repeats (u = nnz, one column per word: column
+    format) share one launch; stencil rows at the block boundaries as well.  Values bit for
+    bit against the oracle (fp32: the SpSGEMM oracle)."""
+    import paper_1504_05022_b200 as sg
+    n = 60_000
+    # B rows 0..199: 24 columns in 3 clusters of 8 consecutive columns; 200..399: 16 columns
+    # 128 apart (one per word)
+    rows, cols = [], []
+    for r in range(200):
+        base = (r * 97) % (n - 3000)
+        for k in range(3):
+            rows += [r] * 8
+            cols += list(range(base + 1000 * k + (r % 32), base + 1000 * k + (r % 32) + 8))
+    for r in range(200, 400):
+        rows += [r] * 16
+        cols += list(20_000 + (r - 200) + 64 * np.arange(16) * 2)
+    B = gen.with_values(gen.from_coo(np.array(rows), np.array(cols), (400, n)), "real", 81)
+    ar, ac = [], []
+    for i in range(64):
+        if i % 2 == 0:
+            js = np.arange(i, i + 6) % 200                    # clustered: word format
+        else:
+            js = 200 + (i * 3) % 60 + np.array([0, 60, 120])   # spread b_j*: words ~ nnz = u
+        ar += [i] * len(js)
+        ac += list(js)
+    A = gen.with_values(gen.from_coo(np.array(ar), np.array(ac), (64, 400)), "real", 82)
+    g = run_gpu(A, B, flags=sg.FLAG_PRECISE, stats=True, fp32=fp32)
+    assert set(g["stats"]["tier_rows"]) == {"bw"}
+    R = oracle.spgemm(A, B, fp32=fp32)
+    np.testing.assert_array_equal(g["rp"], R.rp)
+    np.testing.assert_array_equal(g["ci"], R.ci)
+    vt = np.int32 if fp32 else np.int64
+    np.testing.assert_array_equal(g["val"].view(vt), R.val.view(vt))
