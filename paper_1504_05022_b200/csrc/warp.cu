@@ -814,10 +814,15 @@ __global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLa
     int32_t* oc = a.out_col + o;
     bool words = false;
     if (a.bw_nw) {
-      int nwt = 0;
-      for (int s = 1; s <= nslot; ++s) nwt += __popc(__ballot_sync(kFull, sh_ld(bits + s * kSlotBytes + 4u * lane) != 0u));
-      words = 2 * int64_t(nwt) <= __ldg(a.out_off + row + 1) - o;
-      if (lane == 0) a.bw_nw[row] = words ? nwt : -1;
+      // at most 32 words per slot: count them only when that bound does not settle it
+      const int64_t cap = __ldg(a.out_off + row + 1) - o;
+      words = 64 * int64_t(nslot) <= cap;
+      if (!words) {
+        int nwt = 0;
+        for (int s = 1; s <= nslot; ++s) nwt += __popc(__ballot_sync(kFull, sh_ld(bits + s * kSlotBytes + 4u * lane) != 0u));
+        words = 2 * int64_t(nwt) <= cap;
+      }
+      if (lane == 0 && !words) a.bw_nw[row] = -1;
     }
     int nnz = 0, nl = 0;
     if (words) {
@@ -845,6 +850,7 @@ __global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLa
       }
       nnz = (int)__reduce_add_sync(kFull, pcs);
       bmax = max(bmax, nslot);
+      if (lane == 0) a.bw_nw[row] = nwo;
       if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
       __syncwarp();
       continue;
