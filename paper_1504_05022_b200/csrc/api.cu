@@ -652,28 +652,51 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
     }
     cudaEventRecord(h->tsym[t][0], h->stream);
     if (hybrid && t == T_BW) {
-      // window rows in the hybrid strategy: the structure pass (sorted column sets into the
-      // rows' C~ slices), the exact row-length maximum, then the values by rank (DENSE) into
-      // the same slices — the precise strategy's two walks, with C~ as their output
-      a.mode = MODE_STRUCT;
-      CK(h, launch_stage3_tier(t, a, h->stream));
-      CK(h, cudaMemsetAsync(ws.summary + kSumVmax, 0, sizeof(int64_t), h->stream));
-      k_rows_max<<<256, 256, 0, h->stream>>>(ws.perm, a.first, a.count, h->nnz_row,
-                                              reinterpret_cast<unsigned long long*>(ws.summary + kSumVmax));
-      CK(h, cudaGetLastError());
-      CK(h, cudaMemcpyAsync(h->pinned + kSumVmax, ws.summary + kSumVmax, 2 * sizeof(int64_t),
-                            cudaMemcpyDeviceToHost, h->stream));  // kSumVmax, kSumBmax
-      s = sync(h);
-      if (s != SPGEMM_SUCCESS) return s;
-      a.mode = MODE_DENSE;
-      a.struct_col = h->ctil_col;
-      a.struct_off = ws.ctil_off;
-      a.row_len = h->nnz_row;  // C~ offsets are capacities here
-      a.nnz_row = nullptr;
-      a.bw_vmax = h->pinned[kSumVmax];
-      a.bw_bmax = h->pinned[kSumBmax];
-      CK(h, launch_stage3_tier(t, a, h->stream));
-      h->launches_sym += 2;
+      // window rows in the hybrid strategy: one walk (k_bw_one: insert and accumulate per
+      // product, rows written to their C~ slices in column order); rows with more blocks or
+      // granules than it holds take the two walks — the structure pass (sorted column sets
+      // into the slices), the exact row-length maximum, then the values by rank (DENSE)
+      Stage3Args b = a;
+      int64_t rest = a.count;
+      if (a.b_nnz < (int64_t(1) << 31) && !env_int("SPGEMM_BW_TWO_WALK", 0)) {
+        Stage3Args o1 = a;
+        o1.mode = MODE_FILL;
+        AL(h, &o1.bw_ovf_list, a.count);
+        AL(h, &o1.bw_ovf_cnt, 1);
+        CK(h, launch_bw_one(o1, h->stream));
+        CK(h, cudaMemcpyAsync(h->pinned + kSumLen + 1, o1.bw_ovf_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                              h->stream));
+        s = sync(h);
+        if (s != SPGEMM_SUCCESS) return s;
+        rest = *reinterpret_cast<int32_t*>(h->pinned + kSumLen + 1);
+        b.perm = o1.bw_ovf_list;
+        b.first = 0;
+        b.count = rest;
+        h->launches_sym += 1;
+      }
+      if (rest > 0) {
+        b.mode = MODE_STRUCT;
+        CK(h, launch_stage3_tier(t, b, h->stream));
+        CK(h, cudaMemsetAsync(ws.summary + kSumVmax, 0, sizeof(int64_t), h->stream));
+        k_rows_max<<<256, 256, 0, h->stream>>>(b.perm, b.first, b.count, h->nnz_row,
+                                                reinterpret_cast<unsigned long long*>(ws.summary + kSumVmax));
+        CK(h, cudaGetLastError());
+        CK(h, cudaMemcpyAsync(h->pinned + kSumVmax, ws.summary + kSumVmax, 2 * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, h->stream));  // kSumVmax, kSumBmax
+        s = sync(h);
+        if (s != SPGEMM_SUCCESS) return s;
+        b.mode = MODE_DENSE;
+        b.struct_col = h->ctil_col;
+        b.struct_off = ws.ctil_off;
+        b.row_len = h->nnz_row;  // C~ offsets are capacities here
+        b.nnz_row = nullptr;
+        b.bw_vmax = h->pinned[kSumVmax];
+        b.bw_bmax = h->pinned[kSumBmax];
+        CK(h, launch_stage3_tier(t, b, h->stream));
+        h->launches_sym += 2;
+      } else {
+        --h->launches_sym;
+      }
     } else {
       CK(h, launch_stage3_tier(t, a, h->stream));
     }

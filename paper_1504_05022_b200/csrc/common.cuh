@@ -311,6 +311,7 @@ cudaError_t launch_stage3_tier(int tier, const Stage3Args& a, cudaStream_t s);
 cudaError_t launch_warp_tier(int tier, const Stage3Args& a, cudaStream_t s);
 // window-bitmap class T_BW (warp.cu)
 cudaError_t launch_bw_tier(const Stage3Args& a, cudaStream_t s);
+cudaError_t launch_bw_one(const Stage3Args& a, cudaStream_t s);
 int num_sms();
 // bucket-ESC classes (esc.cu)
 cudaError_t launch_esc(int tier, const Stage3Args& a, cudaStream_t s);

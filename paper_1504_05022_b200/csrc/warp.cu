@@ -909,6 +909,304 @@ __global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLa
     atomicMax(reinterpret_cast<unsigned long long*>(a.bw_bmax_out), (unsigned long long)bmax);
 }
 
+// ----------------------------------------------------------------------------------------
+// T_BW in ONE walk (hybrid strategy, 32-bit B offsets): the dense accumulator of [P:142]
+// restricted to the row's column window, with storage only where the products land.  The
+// window is cut into 1024-column blocks (a directory, slots claimed on first touch, as in
+// k_bw_sym) and each block into 8-column granules; a granule is claimed on first touch and
+// holds 8 values and a presence mask.  Every product is inserted and accumulated in the same
+// step (Algorithm 1 lines 6-11): set its column's bit, add a_ij*b_jk to its value — in
+// j-ascending order per column from -0.0, the oracle's rounding (R1).  At the end
+// the row's granules are sorted by column (one warp bitonic sort of their keys), their
+// popcounts scanned into positions, and each lane writes its granule's entries to the row's
+// C~ slice in order.  No structure pass, no ranks.  A row touching more than kOneSlots blocks
+// or kOneGran granules is listed in bw_ovf_list and goes through the two-walk path
+// (k_bw_sym + k_bwrow DENSE).
+// Per warp: dir u16[nsw] | sblk u16[NS] (block of each slot) | gtab u8[NS*128] (granule of
+// each 8 columns, +1) | gkey u32[NG] | gbits u32[NG] | vals V[8*NG] + scratch | stage 512 B.
+constexpr int kOneSlots = 12;
+constexpr int kOneGran = 56;
+
+struct OneLayout {
+  int nsw;
+  unsigned o_sblk, o_gtab, o_gkey, o_gbits, o_vals, o_stage, o_zero, bytes;
+};
+
+__host__ __device__ inline OneLayout one_layout(int64_t wmax, int vbytes) {
+  OneLayout L;
+  const int nb = (int)(((wmax > 0 ? wmax : 1) + 1023) / 1024);
+  L.nsw = (nb + 31) / 32 * 32;
+  L.o_sblk = (2u * L.nsw + 15u) & ~15u;
+  L.o_gtab = (L.o_sblk + 2u * kOneSlots + 15u) & ~15u;
+  L.o_gkey = (L.o_gtab + 128u * kOneSlots + 15u) & ~15u;
+  L.o_gbits = L.o_gkey + 4u * kOneGran;
+  L.o_zero = (L.o_gbits + 4u * kOneGran + 15u) & ~15u;  // [0, o_zero): zero between rows
+  L.o_vals = L.o_zero;
+  L.o_stage = (L.o_vals + unsigned(vbytes) * (8u * kOneGran + 2u) + 15u) & ~15u;
+  L.bytes = L.o_stage + 512u;
+  return L;
+}
+
+__device__ __forceinline__ unsigned sh_ld_u8(unsigned addr) {
+  unsigned short r;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void sh_st_u8(unsigned addr, unsigned v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
+
+// ascending bitonic sort of 64 keys held two per lane (k0: element lane, k1: element 32+lane)
+__device__ __forceinline__ void warp_sort64(unsigned& k0, unsigned& k1, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+    if (size == 64) {  // the merge across the halves: element i vs i+32, then within halves
+      const unsigned lo = min(k0, k1), hi = max(k0, k1);
+      k0 = lo;
+      k1 = hi;
+    }
+#pragma unroll
+    for (int stride = (size == 64 ? 16 : size / 2); stride > 0; stride >>= 1) {
+      // within each 32-element half, element index i = lane (k0) or 32 + lane (k1)
+      const bool up0 = size == 64 ? true : ((lane & size) == 0);
+      const bool up1 = size == 64 ? true : (((32 + lane) & size) == 0);
+      const unsigned o0 = __shfl_xor_sync(kFull, k0, stride), o1 = __shfl_xor_sync(kFull, k1, stride);
+      const bool lower = (lane & stride) == 0;
+      k0 = (lower == up0) ? min(k0, o0) : max(k0, o0);
+      k1 = (lower == up1) ? min(k1, o1) : max(k1, o1);
+    }
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256, 4) k_bw_one(Stage3Args a, OneLayout L) {
+  extern __shared__ __align__(16) uint32_t s_bw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned dir = (unsigned)__cvta_generic_to_shared(s_bw) + unsigned(w) * L.bytes;
+  const unsigned sblk = dir + L.o_sblk, gtab = dir + L.o_gtab, gkey = dir + L.o_gkey, gbits = dir + L.o_gbits;
+  const unsigned vals = dir + L.o_vals, stage = dir + L.o_stage;
+  const unsigned scratch = vals + unsigned(sizeof(V)) * (8u * kOneGran);
+  const int32_t* __restrict__ aci = a.A.ci;
+  const V* __restrict__ aval = vcast<V>(a.A.val);
+  const int64_t* __restrict__ brp = a.B.rp;
+  const int32_t* __restrict__ bci = a.B.ci;
+  const V* __restrict__ bval = vcast<V>(a.B.val);
+  for (unsigned i = lane; i < L.o_zero / 16u; i += 32) sh_st_v4_zero(dir + 16u * i);
+  for (unsigned i = lane; i < 8u * kOneGran + 2u; i += 32) sh_stv(vals + unsigned(sizeof(V)) * i, V(-0.0));
+  __syncwarp();
+  const unsigned lt = lanemask_lt_();
+
+  const int64_t per = (a.count + gridDim.x - 1) / gridDim.x;  // contiguous rows per CTA (L1 reuse)
+  const int64_t rend = min(int64_t(blockIdx.x) * per + per, a.count);
+  for (int64_t r = int64_t(blockIdx.x) * per + w; r < rend; r += nw) {
+    const int row = __ldg(a.perm + a.first + r);
+    const int lo = __ldg(a.rlo + row);
+    const int64_t a0 = __ldg(a.A.rp + row), a1 = __ldg(a.A.rp + row + 1);
+    int nslot = 0, ngr = 0;  // warp-uniform
+
+    // first touch of blocks, then of granules, for one step (lanes of a b_j* hold ascending
+    // columns, so the lanes needing one new block / granule are contiguous: the first of
+    // each run claims it); sl / gi stay 0 when the row runs out of slots / granules
+    auto claim = [&](unsigned d, bool act, unsigned& sl, unsigned& gi) {
+      const bool nsl = act && sl == 0u;
+      unsigned nm = __ballot_sync(kFull, nsl);
+      if (nm) {
+        const unsigned blk = d >> 10;
+        const unsigned bp = __shfl_up_sync(kFull, blk, 1);
+        const bool lead = nsl && (lane == 0 || !((nm >> (lane - 1)) & 1u) || bp != blk);
+        const unsigned lm = __ballot_sync(kFull, lead);
+        const int id = nslot + __popc(lm & lt) + 1;
+        if (lead && id <= kOneSlots) {
+          sh_st_u16(dir + 2u * blk, (unsigned)id);
+          sh_st_u16(sblk + 2u * (id - 1), blk);
+        }
+        nslot += __popc(lm);
+        __syncwarp();
+        if (nsl) {
+          sl = sh_ld_u16(dir + 2u * blk);
+          if (sl) gi = sh_ld_u8(gtab + (sl - 1u) * 128u + ((d >> 3) & 127u));
+        }
+      }
+      const bool ngl = act && sl != 0u && gi == 0u;
+      nm = __ballot_sync(kFull, ngl);
+      if (nm) {
+        const unsigned key = d >> 3;
+        const unsigned kp = __shfl_up_sync(kFull, key, 1);
+        const bool lead = ngl && (lane == 0 || !((nm >> (lane - 1)) & 1u) || kp != key);
+        const unsigned lm = __ballot_sync(kFull, lead);
+        const int id = ngr + __popc(lm & lt) + 1;
+        if (lead && id <= kOneGran) {
+          sh_st_u8(gtab + (sl - 1u) * 128u + (key & 127u), (unsigned)id);
+          sh_st(gkey + 4u * (id - 1), key);
+        }
+        ngr += __popc(lm);
+        __syncwarp();
+        if (ngl) gi = sh_ld_u8(gtab + (sl - 1u) * 128u + (key & 127u));
+      }
+    };
+    // line 8 (insert: the column's bit) and lines 9 / 11 (accumulate) of one product
+    auto insert_add = [&](unsigned d, unsigned gi, V pr) {
+      if (gi) sh_red_or(gbits + 4u * (gi - 1u), 1u << (d & 7u));
+      const unsigned va = gi ? vals + unsigned(sizeof(V)) * ((gi - 1u) * 8u + (d & 7u)) : scratch;
+      sh_stv(va, Arith<V>::add(sh_ldv<V>(va), pr));
+      __syncwarp();  // the next step's lanes may read this slot
+    };
+
+    bool fail = false;
+    for (int64_t e0 = a0; e0 < a1 && !fail; e0 += 32) {
+      const int64_t e = e0 + lane;
+      int bs = 0, len = 0;
+      V av = V(0);
+      if (e < a1) {
+        const int j = __ldg(aci + e);
+        const int64_t b0 = __ldg(brp + j);
+        bs = (int)b0;
+        len = (int)(__ldg(brp + j + 1) - b0);
+        av = __ldg(aval + e);
+      }
+      const double avd = (double)av;
+      const int lo_w = sizeof(V) == 8 ? __double2loint(avd) : __float_as_int((float)av);
+      const int hi_w = sizeof(V) == 8 ? __double2hiint(avd) : 0;
+      __syncwarp();
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stage + 16u * lane), "r"(bs), "r"(len),
+                   "r"(lo_w), "r"(hi_w) : "memory");
+      __syncwarp();
+      const int nE = (int)min(int64_t(32), a1 - e0);
+      if (__any_sync(kFull, len > 32)) {
+        for (int t = 0; t < nE && !fail; ++t) {
+          int4 rr;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(rr.x), "=r"(rr.y), "=r"(rr.z), "=r"(rr.w) : "r"(stage + 16u * t) : "memory");
+          const V at = rec_val<V>(rr);
+          for (int q0 = 0; q0 < rr.y; q0 += 32) {
+            const bool act = q0 + lane < rr.y;
+            const int q = rr.x + q0 + lane;
+            const unsigned d = act ? (unsigned)(__ldg(bci + q) - lo) : 0u;
+            const V pr = act ? Arith<V>::mul(at, __ldg(bval + q)) : V(0);
+            unsigned sl = act ? sh_ld_u16(dir + 2u * (d >> 10)) : 0u;
+            unsigned gi = sl ? sh_ld_u8(gtab + (sl - 1u) * 128u + ((d >> 3) & 127u)) : 0u;
+            claim(d, act, sl, gi);
+            if (nslot > kOneSlots || ngr > kOneGran) {
+              fail = true;
+              break;
+            }
+            insert_add(d, gi, pr);
+          }
+        }
+        continue;
+      }
+      for (int t0 = 0; t0 < nE; t0 += kGroup) {
+        unsigned d[kGroup], sl[kGroup], gi[kGroup];
+        V pr[kGroup];
+        bool act[kGroup];
+        bool need = false;
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          int4 rr;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(rr.x), "=r"(rr.y), "=r"(rr.z), "=r"(rr.w) : "r"(stage + 16u * (t0 + u)) : "memory");
+          act[u] = lane < rr.y;
+          const int q = rr.x + min(lane, max(rr.y - 1, 0));
+          const int c = __ldg(bci + q);
+          pr[u] = Arith<V>::mul(rec_val<V>(rr), __ldg(bval + q));
+          d[u] = act[u] ? (unsigned)(c - lo) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          sl[u] = act[u] ? sh_ld_u16(dir + 2u * (d[u] >> 10)) : 0u;
+          gi[u] = sl[u] ? sh_ld_u8(gtab + (sl[u] - 1u) * 128u + ((d[u] >> 3) & 127u)) : 0u;
+          need = need || (act[u] && gi[u] == 0u);
+        }
+        if (__any_sync(kFull, need)) {
+          // first touches, step by step in walk order; a later step of the group may hit the
+          // same new block / granule, so its lookups are refreshed after each claim
+#pragma unroll
+          for (int u = 0; u < kGroup; ++u) {
+            claim(d[u], act[u], sl[u], gi[u]);
+#pragma unroll
+            for (int v2 = u + 1; v2 < kGroup; ++v2)
+              if (act[v2] && gi[v2] == 0u) {
+                sl[v2] = sh_ld_u16(dir + 2u * (d[v2] >> 10));
+                gi[v2] = sl[v2] ? sh_ld_u8(gtab + (sl[v2] - 1u) * 128u + ((d[v2] >> 3) & 127u)) : 0u;
+              }
+          }
+          if (nslot > kOneSlots || ngr > kOneGran) {
+            fail = true;
+            break;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) insert_add(d[u], gi[u], pr[u]);
+      }
+    }
+    __syncwarp();
+    const int ns = min(nslot, kOneSlots), ng = min(ngr, kOneGran);
+    if (!fail) {
+      // the row's granules in column order: sort (key << 8 | granule), scan the popcounts
+      unsigned k0 = lane < ng ? (sh_ld(gkey + 4u * lane) << 8) | unsigned(lane) : 0xffffffffu;
+      unsigned k1 = 32 + lane < ng ? (sh_ld(gkey + 4u * (32 + lane)) << 8) | unsigned(32 + lane) : 0xffffffffu;
+      if (ng > 32) {
+        warp_sort64(k0, k1, lane);
+      } else {
+        // 32 keys: the first half of the network
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+          for (int stride = size / 2; stride > 0; stride >>= 1) {
+            const unsigned o0 = __shfl_xor_sync(kFull, k0, stride);
+            const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+            k0 = (lower == up) ? min(k0, o0) : max(k0, o0);
+          }
+      }
+      const unsigned b0 = k0 != 0xffffffffu ? sh_ld(gbits + 4u * (k0 & 0xffu)) : 0u;
+      const unsigned b1 = k1 != 0xffffffffu ? sh_ld(gbits + 4u * (k1 & 0xffu)) : 0u;
+      const int p0c = __popc(b0), p1c = __popc(b1);
+      const int inc0 = warp_incl_scan(p0c, lane);
+      const int tot0 = __shfl_sync(kFull, inc0, 31);
+      const int inc1 = warp_incl_scan(p1c, lane);
+      const int nnz = tot0 + __shfl_sync(kFull, inc1, 31);
+      // each lane writes its granules' entries at their positions, restoring the values to
+      // -0.0 and the masks to 0 behind it
+      const int64_t o = __ldg(a.out_off + row);
+      int32_t* oc = a.out_col + o;
+      V* ov = vcast<V>(a.out_val) + o;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned kk = h ? k1 : k0;
+        unsigned wd = h ? b1 : b0;
+        int p = h ? tot0 + inc1 - p1c : inc0 - p0c;
+        if (kk != 0xffffffffu) {
+          const unsigned g = kk & 0xffu;
+          const int cb = lo + (int)((kk >> 8) << 3) - 1;
+          const unsigned vb = vals + unsigned(sizeof(V)) * (8u * g);
+          sh_st(gbits + 4u * g, 0u);
+          while (wd) {
+            const int f = __ffs(wd);
+            wd &= wd - 1;
+            const unsigned va = vb + unsigned(sizeof(V)) * unsigned(f - 1);
+            oc[p] = cb + f;
+            ov[p] = sh_ldv<V>(va);
+            sh_stv(va, V(-0.0));
+            ++p;
+          }
+        }
+      }
+      if (lane == 0) a.nnz_row[row] = nnz;
+    } else {
+      // out of slots or granules: restore the cleared state, hand the row to the two-walk path
+      for (int g = lane; g < ng; g += 32) {
+        sh_st(gbits + 4u * g, 0u);
+        for (int k = 0; k < 8; ++k) sh_stv(vals + unsigned(sizeof(V)) * (8u * g + k), V(-0.0));
+      }
+      if (lane == 0) a.bw_ovf_list[atomicAdd(a.bw_ovf_cnt, 1)] = row;
+    }
+    // directory entries of the row's blocks and their granule tables
+    if (lane < ns) sh_st_u16(dir + 2u * sh_ld_u16(sblk + 2u * lane), 0u);
+    for (int i = lane; i < ns * 8; i += 32) sh_st_v4_zero(gtab + 16u * i);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 template <typename K>
@@ -1020,6 +1318,29 @@ static cudaError_t launch_sym(const Stage3Args& a, cudaStream_t s) {
   const int64_t need = (a.count + nw - 1) / nw;
   const int64_t cap = int64_t(num_sms()) * per_sm;
   k_bw_sym<<<(unsigned)(need < cap ? need : cap), nw * 32, bytes, s>>>(a, L);
+  return cudaGetLastError();
+}
+
+// Hybrid window rows in one walk (k_bw_one); rows out of slots or granules are listed in
+// a.bw_ovf_list / a.bw_ovf_cnt (zeroed here) for the two-walk path.
+cudaError_t launch_bw_one(const Stage3Args& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const OneLayout L = one_layout(a.bw_wmax, a.f32 ? 4 : 8);
+  auto kern = a.f32 ? k_bw_one<float> : k_bw_one<double>;
+  constexpr int nw = 8;
+  const size_t bytes = size_t(nw) * L.bytes;
+  if (bytes > 227 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaMemsetAsync(a.bw_ovf_cnt, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.count + nw - 1) / nw;
+  const int64_t cap = int64_t(num_sms()) * per_sm;
+  kern<<<(unsigned)(need < cap ? need : cap), nw * 32, bytes, s>>>(a, L);
   return cudaGetLastError();
 }
 
