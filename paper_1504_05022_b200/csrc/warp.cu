@@ -306,7 +306,7 @@ __device__ __forceinline__ void sh_st_v4_zero(unsigned addr) {
 //   vals double[nv]
 struct BwLayout {
   int nwd, nsw, nvp, nv, ns;
-  unsigned o_sm, o_pre, o_lst, o_vals, o_stage, o_cols, bytes;  // per warp, bytes: multiple of 16
+  unsigned o_sm, o_pre, o_lst, o_vals, o_stage, bytes;  // per warp, bytes is a multiple of 16
 };
 
 constexpr unsigned kRecSlot = 264u;  // DENSE: bytes per slot of 8-byte word records (33 records)
@@ -331,16 +331,12 @@ __host__ __device__ inline BwLayout bw_layout(int mode, int64_t wmax, int64_t vm
     off = (off + 15u) & ~15u;
     L.o_stage = off;         // a_ij chunk records of walk_row_staged
     off += 512u;
-    L.o_cols = off;          // C's columns of a row given as words (written in order with vals)
-#ifdef SG_COLS_SMEM
-    off += 4u * L.nvp;
-#endif
   } else {  // STRUCT: bitmap + summary
     L.o_stage = 0;
     off = 4u * L.nwd;
     L.o_sm = off;
     off += 4u * L.nsw;
-    L.o_pre = L.o_lst = L.o_vals = L.o_cols = off;
+    L.o_pre = L.o_lst = L.o_vals = off;
   }
   L.bytes = (off + 15u) & ~15u;
   return L;
@@ -420,7 +416,7 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
       __syncwarp();
       continue;
     }
-    const unsigned dir = sm, bits = lst, cols = bm + L.o_cols;  // DENSE names
+    const unsigned dir = sm, bits = lst;  // DENSE names
     int nslot = 0, nwr = -1;
     if (MODE == MODE_DENSE) {
       // the sorted column set from the symbolic pass: slots of the nonzero blocks in column
@@ -431,7 +427,7 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
       if (nwr >= 0) {
         // the row as its nonzero words (first column, bits), ascending: a word's record is
         // {bits, rank of its first bit} with the rank from one scan of the popcounts; the
-        // columns go to the warp's column buffer at their ranks (written out with the values)
+        // word's columns go to C at their ranks
         const uint2* sw = reinterpret_cast<const uint2*>(sc);
         int prevb = -1, rank0 = 0;
         for (int p0 = 0; p0 < nwr; p0 += 32) {
@@ -454,20 +450,11 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
                          "r"(ent.y), "r"((unsigned)rank));
             unsigned wd = ent.y;
             const int cb = (int)ent.x - 1;
-#ifdef SG_COLS_SMEM
-            unsigned ca = cols + 4u * unsigned(rank);
-            while (wd) {
-              sh_st(ca, (unsigned)(cb + __ffs(wd)));
-              ca += 4u;
-              wd &= wd - 1;
-            }
-#else
-            int32_t* q = a.out_col + o + rank;
+            int32_t* q = a.out_col + o + rank;  // C's columns of the word, at their ranks
             while (wd) {
               *q++ = cb + __ffs(wd);
               wd &= wd - 1;
             }
-#endif
           }
           nslot += __popc(nm);
           prevb = __shfl_sync(kFull, blk, 31);
@@ -528,18 +515,7 @@ __global__ void __launch_bounds__(256, SG_BW_MINB) k_bwrow(Stage3Args a, BwLayou
     walk_any<true, IT, V>(a, a0, a1, lane, bm + L.o_stage, accumulate);
     __syncwarp();
     V* ov = vcast<V>(a.out_val) + o;
-#ifdef SG_COLS_SMEM
-    if (nwr >= 0) {
-      int32_t* oc = a.out_col + o;
-      for (int p = lane; p < nnz; p += 32) {
-        oc[p] = (int)sh_ld(cols + 4u * p);
-        ov[p] = sh_ldv<V>(vals + 8u * p);
-      }
-    } else
-#endif
-    {
-      for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
-    }
+    for (int p = lane; p < nnz; p += 32) ov[p] = sh_ldv<V>(vals + 8u * p);
     for (int s = 0; s < nslot; ++s) sh_st(bits + unsigned(s) * kRecSlot + 8u * lane, 0u);
     for (int q = lane; q < (2 * nsw) / 16; q += 32) sh_st_v4_zero(dir + 16u * q);
     if (lane == 0 && a.nnz_row) a.nnz_row[row] = nnz;
