@@ -172,8 +172,9 @@ spgemm_status_t spgemm_set_debug_long_bucket(int64_t min_window);
 
 /* Workspace comes from a library-owned stream-ordered memory pool per device that keeps
  * freed blocks cached (warm multiplies make no OS allocations; the device's default pool and
- * PyTorch's allocator are not touched).  This returns cached bytes above keep_bytes to the
- * device (current device; synchronises it).  Errors: CUDA. */
+ * PyTorch's allocator are not touched); the hybrid long-row VMM arenas are cached likewise
+ * (up to 4, with their mapped pages).  This releases every cached arena and returns pool
+ * bytes above keep_bytes to the device (current device; synchronises it).  Errors: CUDA. */
 spgemm_status_t spgemm_trim_workspace_cache(int64_t keep_bytes);
 
 const char* spgemm_status_string(spgemm_status_t s);

@@ -196,6 +196,12 @@ spgemm_status_t dalloc(spgemm_handle_t h, T** p, int64_t count) {
   const size_t bytes = sizeof(T) * size_t(count > 0 ? count : 1);
   void* q = nullptr;
   cudaError_t e = pool_malloc(&q, bytes, h->stream);
+  if (e == cudaErrorMemoryAllocation) {  // cached long-row arenas hold pages: release, retry
+    cudaGetLastError();
+    cudaStreamSynchronize(h->stream);
+    vmm_trim();
+    e = pool_malloc(&q, bytes, h->stream);
+  }
   if (e != cudaSuccess) return cuda_fail(h, e, "cudaMallocFromPoolAsync");
   h->allocs.emplace_back(q, bytes);
   h->bytes += bytes;
@@ -1017,6 +1023,7 @@ spgemm_status_t spgemm_trim_workspace_cache(int64_t keep_bytes) {
   cudaMemPool_t pool = library_pool(dev);
   if (!pool) return fail(nullptr, SPGEMM_ERROR_CUDA, "no library memory pool");
   cudaDeviceSynchronize();
+  vmm_trim();  // the cached long-row arenas (vmm.cu)
   cudaError_t e = cudaMemPoolTrimTo(pool, keep_bytes > 0 ? (size_t)keep_bytes : 0);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMemPoolTrimTo");
   return SPGEMM_SUCCESS;

@@ -396,7 +396,8 @@ struct VmmArena {
 };
 cudaError_t vmm_reserve(VmmArena* a, size_t bytes);
 cudaError_t vmm_ensure(VmmArena* a, size_t bytes);
-void vmm_release(VmmArena* a);
+void vmm_release(VmmArena* a);  // back to the per-device cache (at most 4 arenas kept)
+void vmm_trim();                  // release the cached arenas
 
 // Stage 4 -------------------------------------------------------------------------------
 struct CopyArgs {

@@ -76,10 +76,33 @@ cudaError_t cu_err(CUresult r) {
 
 }  // namespace
 
+// Released arenas are kept (reservation and mapped pages) for the next multiply on the device,
+// like the library's memory pool keeps freed workspace: mapping and unmapping tens of GB of
+// physical pages per multiply is host time inside the step.  spgemm_trim_workspace_cache
+// releases them (vmm_trim).
+static std::mutex g_cache_mu;
+static std::vector<VmmArena> g_cache;
+
+static void release_now(VmmArena* a);
+
 cudaError_t vmm_reserve(VmmArena* a, size_t bytes) {
   const DriverVmm& d = drv();
   if (!d.ok) return cudaErrorNotSupported;
   cudaGetDevice(&a->device);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_cache.size(); ++i)
+      if (g_cache[i].device == a->device && g_cache[i].reserved >= bytes &&
+          (best < 0 || g_cache[i].reserved < g_cache[best].reserved))
+        best = i;
+    if (best >= 0) {
+      *a = g_cache[best];
+      g_cache.erase(g_cache.begin() + best);
+      return cudaSuccess;
+    }
+  }
+  vmm_trim();  // no cached arena fits: do not keep pages for ones that will not be reused
   CUmemAllocationProp p = props(a->device);
   size_t g = 0;
   CUresult r = d.gran(&g, &p, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
@@ -110,6 +133,10 @@ cudaError_t vmm_ensure(VmmArena* a, size_t bytes) {
   CUmemAllocationProp p = props(a->device);
   CUmemGenericAllocationHandle h;
   CUresult r = d.create(&h, size, &p, 0);
+  if (r == CUDA_ERROR_OUT_OF_MEMORY) {  // pages held by cached arenas: release them, retry
+    vmm_trim();
+    r = d.create(&h, size, &p, 0);
+  }
   if (r != CUDA_SUCCESS) return cu_err(r);
   const CUdeviceptr at = reinterpret_cast<CUdeviceptr>(a->base) + a->mapped;
   r = d.map(at, size, 0, h, 0);
@@ -134,6 +161,28 @@ cudaError_t vmm_ensure(VmmArena* a, size_t bytes) {
 }
 
 void vmm_release(VmmArena* a) {
+  if (!a->base) return;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (g_cache.size() < 4) {
+      g_cache.push_back(*a);
+      *a = VmmArena{};
+      return;
+    }
+  }
+  release_now(a);
+}
+
+void vmm_trim() {
+  std::vector<VmmArena> all;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    all.swap(g_cache);
+  }
+  for (auto& a : all) release_now(&a);
+}
+
+static void release_now(VmmArena* a) {
   if (!a->base) return;
   const DriverVmm& d = drv();
   Impl* im = static_cast<Impl*>(a->impl);

@@ -609,3 +609,26 @@ def test_window_rows_word_and_column_structure(fp32):
     np.testing.assert_array_equal(g["ci"], R.ci)
     vt = np.int32 if fp32 else np.int64
     np.testing.assert_array_equal(g["val"].view(vt), R.val.view(vt))
+
+
+def test_long_arena_cache_reuse():
+    """The hybrid long-row VMM arenas are kept for the next multiply (mapped pages and stale
+    data included): back-to-back progressive multiplies of different sizes, then again after
+    trim_workspace_cache released them — every result equals the oracle bit for bit."""
+    import paper_1504_05022_b200 as sg
+    cases = []
+    for k, (u, dup) in enumerate([(5000, 0.0), (1500, 0.5), (5000, 0.95)]):
+        A, B = gen.forced_u_pair([u, u // 2, 700, u], n=60000, seed=900 + k, mode="real", dup=dup)
+        cases.append((A, B, oracle.spgemm(A, B)))
+    try:
+        sg.set_debug(-1, 64, 40)  # long path for cap > 40, initial capacity 64: growth rounds
+        for rnd in range(2):
+            for A, B, R in cases:
+                g = run_gpu(A, B, stats=True)
+                assert g["stats"]["long_rows"] == 4
+                np.testing.assert_array_equal(g["rp"], R.rp)
+                np.testing.assert_array_equal(g["ci"], R.ci)
+                np.testing.assert_array_equal(g["val"].view(np.int64), R.val.view(np.int64))
+            sg.trim_workspace_cache(0)
+    finally:
+        sg.set_debug(-1, 0, 0)

@@ -1,0 +1,7 @@
+#!/bin/bash
+OUT=gpurun_out/${TAG:-r2o}; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "bw or window or stencil or config1 or strategies or c2_full or galerkin" > $OUT/tests.log 2>&1; echo TESTS_RC=$? >> $OUT/tests.log
+tail -2 $OUT/tests.log
+bash tools/ab2.sh ${TAG:-r2o} "libspgemm.so libspgemm_sym256.so libspgemm_sym64.so" "c2 g3d27" precise
+bash tools/ab2.sh ${TAG:-r2o}h "libspgemm.so libspgemm_one256.so" "c2" hybrid
