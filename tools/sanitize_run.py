@@ -46,4 +46,31 @@ for fl in (0, sg.FLAG_PRECISE):
     check(A, B, fl, what="long multi-tile / bucket flags=%d" % fl)
 sg.set_debug_long_bucket(1)
 check(A, B, sg.FLAG_PRECISE, what="long bucket path (all long rows)")
+sg.set_debug_long_bucket(0)
+sg.set_debug_long_tile(0)
+sg.set_debug(-1, 0, 0)
+# window class: word-format and column-format structure rows (precise), k_bw_one rows and its
+# overflow rows (> 56 granules: the two-walk fallback) in the hybrid strategy
+n = 60_000
+rows, cols = [], []
+for r in range(200):
+    base = (r * 97) % (n - 3000)
+    for k in range(3):
+        rows += [r] * 8
+        cols += list(range(base + 1000 * k + (r % 32), base + 1000 * k + (r % 32) + 8))
+for r in range(200, 400):
+    rows += [r] * 16
+    cols += list(20_000 + (r - 200) + 128 * np.arange(16))
+Bw = gen.with_values(gen.from_coo(np.array(rows), np.array(cols), (400, n)), "real", 81)
+ar, ac = [], []
+for i in range(96):
+    js = (np.arange(i, i + 6) % 200 if i % 3 == 0 else
+          200 + (i * 3) % 60 + np.array([0, 60, 120]) if i % 3 == 1 else
+          200 + (i * 3) % 40 + np.array([0, 30, 60, 90, 120]))
+    ar += [i] * len(js)
+    ac += list(js)
+Aw = gen.with_values(gen.from_coo(np.array(ar), np.array(ac), (96, 400)), "real", 82)
+for fl in (0, sg.FLAG_PRECISE):
+    check(Aw, Bw, fl, what="window word/column/overflow rows flags=%d" % fl)
+    check(Aw, Bw, fl, fp32=True, what="window rows fp32 flags=%d" % fl)
 print("SANITIZE_RUN_DONE")
