@@ -409,7 +409,7 @@ def measure(args, ctx, cfg, strategy, steps, warmup, clocks_on=True, variant="i"
             if c["ms"] <= 0:
                 continue
             alg = 16 * c["rows"] + 12 * c["a_entries"] + 12 * min(Bm0.nnz, c["products"]) + 12 * c["c_entries"]
-            kname = ("k_bwrow DENSE" if not hybrid else "k_bw_sym + k_bwrow DENSE") if cls_name == "bw" else \
+            kname = ("k_bwrow DENSE" if not hybrid else "k_bw_one") if cls_name == "bw" else \
                 "k_esc_bk" if cls_name.startswith(("w", "e")) else \
                 "k_group" if cls_name.startswith("g") else \
                 "k_long_rank" if cls_name.startswith("c") else "k_bk_part/sort/copy + k_long_rank"

@@ -1092,17 +1092,19 @@ __global__ void __launch_bounds__(256, 4) k_bw_one(Stage3Args a, OneLayout L) {
           need = need || (act[u] && gi[u] == 0u);
         }
         if (__any_sync(kFull, need)) {
-          // first touches, step by step in walk order; a later step of the group may hit the
-          // same new block / granule, so its lookups are refreshed after each claim
+          // first touches, step by step in walk order; a later step of the group may hit a
+          // block / granule claimed by an earlier one, so its lookups are refreshed (once,
+          // just before its own claims) when the group has claimed anything so far
+          bool claimed = false;  // warp-uniform
 #pragma unroll
           for (int u = 0; u < kGroup; ++u) {
+            if (claimed && act[u] && gi[u] == 0u) {
+              sl[u] = sh_ld_u16(dir + 2u * (d[u] >> 10));
+              gi[u] = sl[u] ? sh_ld_u8(gtab + (sl[u] - 1u) * 128u + ((d[u] >> 3) & 127u)) : 0u;
+            }
+            const int ns0 = nslot, ng0 = ngr;
             claim(d[u], act[u], sl[u], gi[u]);
-#pragma unroll
-            for (int v2 = u + 1; v2 < kGroup; ++v2)
-              if (act[v2] && gi[v2] == 0u) {
-                sl[v2] = sh_ld_u16(dir + 2u * (d[v2] >> 10));
-                gi[v2] = sl[v2] ? sh_ld_u8(gtab + (sl[v2] - 1u) * 128u + ((d[v2] >> 3) & 127u)) : 0u;
-              }
+            claimed = claimed || nslot != ns0 || ngr != ng0;
           }
           if (nslot > kOneSlots || ngr > kOneGran) {
             fail = true;
