@@ -498,10 +498,10 @@ def run_gpu(args):
     if world == 1 and not args.no_per_config:
         per = {}
         for cfg in PER_CONFIG:
-            # both strategies where they trade places: c2 (precise ahead: r_c = 5.8, C~ 6x C),
-            # c3a / c3b (power law: hybrid saves the counting pass where r_c is near 1), c4a / c4b
-            # (A·P rows of at most 32 products: hybrid saves the count, R·(AP) is a window product)
-            for strat in (["precise", "hybrid"] if cfg in ("c2", "c3a", "c3b", "c4a", "c4b") else ["precise"]):
+            # both strategies: they trade places — c2 (precise ahead: r_c = 5.8, C~ 6x C), c3a
+            # (power law: hybrid saves the counting pass where r_c is near 1), c4a / c4b and the
+            # Galerkin hierarchies (A·P rows of at most 32 products: hybrid saves the count)
+            for strat in ["precise", "hybrid"]:
                 if cfg == args.config and strat == args.strategy:
                     continue
                 torch.cuda.empty_cache()

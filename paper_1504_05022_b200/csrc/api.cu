@@ -592,7 +592,10 @@ spgemm_status_t spgemm_symbolic(spgemm_handle_t h, int64_t* c_nnz) {
   AL(h, &h->scan_tmp, scan_tmp_elems(m > (1 << 20) ? m : (1 << 20)));
   // nnz(c_i*) = 0 for rows that never reach a stage-3 kernel (u_i = 0: bin group 1 [P:216])
   CK(h, cudaMemsetAsync(h->nnz_row, 0, sizeof(int64_t) * m, h->stream));
-  TierParams tp{g_force_tier, g_long_threshold, g_bk_min_w, precise ? 1 : 0};
+  // window class by the relaxed bound in both strategies: precise re-bins rows longer than
+  // kBwMaxV after the count; hybrid rows that outgrow k_bw_one's granules take the two walks
+  // (g3d27 hierarchy hybrid 59 -> 17.6 ms, g3d7 12.3 -> 6.8; g2d9 5.4 -> 5.9, (PᵀA)P 43 -> 52)
+  TierParams tp{g_force_tier, g_long_threshold, g_bk_min_w, env_int("SPGEMM_BW_STRICT", 0) ? 0 : 1};
   h->bk_min_w = g_bk_min_w;
   tp.force_tier = env_int("SPGEMM_FORCE_TIER", tp.force_tier);
   for (int t = 0; t < NUM_TIERS; ++t) h->tev_used[t] = h->tsym_used[t] = false;

@@ -58,7 +58,7 @@ struct TierParams {
   int force_tier;         // -1 = off
   int64_t long_threshold; // rows with cap above go long (0 = default by smem)
   int64_t bk_min_w;       // precise long rows: window above which values take the bucket path
-  int bw_relax;           // precise: window rows by the relaxed bound (kBwMaxVRelax)
+  int bw_relax;           // window rows by the relaxed bound (kBwMaxVRelax)
 };
 
 // Long rows, precise numeric: rows whose column window is wider than one bitmap tile of the

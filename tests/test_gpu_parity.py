@@ -89,7 +89,7 @@ def _classify(u, n, W):
         while (1 << g) < u:
             g += 1
         return 1 + g
-    if 0 < W <= (1 << 17) and min(cap, W) <= 2048:   # window bitmap
+    if 0 < W <= (1 << 17) and min(cap, W) <= 8192:   # window bitmap (the relaxed bound, both strategies)
         return 19
     for t in range(7, 13):
         if 4 * (64 << (t - 7)) >= 5 * cap:
@@ -526,8 +526,9 @@ def test_long_bucket_path(mode, min_window, flags_name):
 def test_window_class_relaxed_bound(flags_name):
     """Precise strategy: rows with 2048 < min(u, W) <= 8192 and W <= 2^17 start in the window
     class; after the count, those longer than 2048 leave it for the ESC / CTA classes, the rest
-    (columns repeated by many b_j*) keep the dense accumulator.  Hybrid keeps the strict bound.
-    Structure exact, values bit for bit against the oracle."""
+    (columns repeated by many b_j*) keep the dense accumulator.  Hybrid takes the same bound:
+    its one-walk kernel keeps the rows whose granules fit, the others take the two walks into
+    their C~ slices.  Structure exact, values bit for bit against the oracle."""
     import paper_1504_05022_b200 as sg
     flags = getattr(sg, flags_name) if flags_name else 0
     n = 100_000
