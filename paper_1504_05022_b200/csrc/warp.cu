@@ -701,22 +701,10 @@ __global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLa
       asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(stage + 8u * lane), "r"(bs), "r"(len) : "memory");
       __syncwarp();
       const int nE = (int)min(int64_t(32), a1 - e0);
+      const bool chunk_long = __any_sync(kFull, len > 32);  // one vote per 32 a_ij
       for (int t0 = 0; t0 < nE; t0 += kGroup) {
-        unsigned d[kGroup], sl[kGroup];
-        bool need[kGroup];
-        int nlong = 0;
-#pragma unroll
-        for (int u = 0; u < kGroup; ++u) {
-          const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));  // lanes past the row: len 0
-          nlong |= (int)rec.y > 32;
-          const bool act = lane < (int)rec.y;
-          const int q = (int)rec.x + lane;  // 32-bit index: one IMAD.WIDE per gather
-          d[u] = act ? (unsigned)(__ldg(bci + q) - lo) : 0u;
-          sl[u] = act ? sh_ld_u16(dir + 2u * (d[u] >> 10)) : 0u;  // 0: dummy slot / no slot yet
-          need[u] = act && sl[u] == 0u;
-        }
-        if (__any_sync(kFull, nlong)) {
-          // a b_j* longer than 32 in this group: take the general path for the whole group
+        if (chunk_long) {
+          // a b_j* longer than 32 in this chunk: the general path for its groups
           for (int u = 0; u < kGroup && t0 + u < nE; ++u) {
             const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));
             for (int q0 = 0; q0 < (int)rec.y; q0 += 32) {
@@ -740,6 +728,17 @@ __global__ void __launch_bounds__(256, SG_SYM_MINB) k_bw_sym(Stage3Args a, SymLa
             }
           }
           continue;
+        }
+        unsigned d[kGroup], sl[kGroup];
+        bool need[kGroup];
+#pragma unroll
+        for (int u = 0; u < kGroup; ++u) {
+          const uint2 rec = sh_ld_v2(stage + 8u * (t0 + u));  // lanes past the row: len 0
+          const bool act = lane < (int)rec.y;
+          const int q = (int)rec.x + lane;  // 32-bit index: one IMAD.WIDE per gather
+          d[u] = act ? (unsigned)(__ldg(bci + q) - lo) : 0u;
+          sl[u] = act ? sh_ld_u16(dir + 2u * (d[u] >> 10)) : 0u;  // 0: dummy slot / no slot yet
+          need[u] = act && sl[u] == 0u;
         }
         const bool any_need = need[0] || need[1] || need[2] || need[3];
         if (__any_sync(kFull, any_need)) {
